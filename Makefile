@@ -1,0 +1,22 @@
+# Build libsldg.so for B200 (sm_100a).  `python -c "import __graft_entry__ as g; g.build()"`
+# runs the same recipe.
+NVCC ?= nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -O3 \
+           -Iinclude -Ipaper_2603_19959_b200/csrc --expt-relaxed-constexpr
+SRCS := $(wildcard paper_2603_19959_b200/csrc/*.cu)
+LIB := paper_2603_19959_b200/_lib/libsldg.so
+
+all: $(LIB)
+
+$(LIB): $(SRCS) $(wildcard paper_2603_19959_b200/csrc/*.cuh) include/sldg_capi.h
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS)
+
+ptxas:
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /tmp/sldg_probe.o paper_2603_19959_b200/csrc/vsweep.cu
+
+clean:
+	rm -f $(LIB)
+
+.PHONY: all clean ptxas

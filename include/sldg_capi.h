@@ -1,0 +1,180 @@
+/*
+ * sldg_capi.h -- C ABI of the B200-native SLDG transport step (libsldg.so).
+ *
+ * Plain pointers and sizes only; no torch types.  Every entry point returns
+ * an int status (SLDG_OK == 0); on failure sldg_last_error() returns a
+ * thread-local message.  Device pointers are caller-owned (fp64, row-major,
+ * row = one velocity DOF, x fastest, leading dimension `ld` in elements).
+ * Per-step entry points never allocate, never synchronise the host and
+ * enqueue on the given stream (a cudaStream_t passed as void*; NULL = legacy
+ * default stream).  Plans own their device memory.
+ *
+ * Reference interfaces replaced (all /root/reference/pkg/src/sldg_vlasov/):
+ *   sldg_vplan_create       <- vsweep.build_sweep_plan          vsweep.py:307-387
+ *                              (+ pencil.extract_pencils/classify_conforming arrays,
+ *                               pencil.py:60-168, uploaded once)
+ *   sldg_advect_v           <- vsweep.advect_velocity            vsweep.py:413-441
+ *                              (_sweep_column 390-410, sweep_pencil 173-246,
+ *                               weighted_writeback 249-272, precompute_level_matrices 47-61)
+ *   sldg_level_matrices     <- vsweep.precompute_level_matrices  vsweep.py:47-61
+ *                              (decompose_shift sldg1d.py:39-55, overlap_pair sldg1d.py:82-100)
+ *   sldg_xplan_create       <- xfield.precompute_x_matrices      xfield.py:63-79
+ *   sldg_advect_x           <- xfield.advect_x                   xfield.py:82-104
+ *   sldg_rho                <- xfield.compute_rho                xfield.py:107-109
+ *   sldg_poisson_create     <- xfield.PoissonSolver.__init__     xfield.py:121-146
+ *   sldg_poisson_solve      <- PoissonSolver.solve + electric_field  xfield.py:148-179
+ *   sldg_moments            <- driver.moments                    driver.py:139-146
+ *   sldg_field_diag         <- xfield.field_energy + max|E|      xfield.py:192-195, driver.py:220-229
+ */
+#ifndef SLDG_CAPI_H
+#define SLDG_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLDG_OK 0
+#define SLDG_ERR_ARG 1      /* bad argument / shape (SweepError / ValueError in Python) */
+#define SLDG_ERR_CUDA 2     /* CUDA runtime failure */
+#define SLDG_ERR_PLAN 3     /* inconsistent plan (uncovered DOFs, bad CSR) */
+#define SLDG_ERR_UNSUPPORTED 4
+
+#define SLDG_BC_PERIODIC 0
+#define SLDG_BC_ABSORBING 1
+
+#define SLDG_MAX_DEGREE 5   /* p <= 5 (o = p+1 <= 6) compiled */
+
+/* Reference element constants (basis.DGBasis, basis.py:84-148). */
+typedef struct SldgBasis {
+  int32_t degree;             /* p */
+  const double* nodes;        /* p+1 GLL nodes */
+  const double* inv_denoms;   /* p+1 Lagrange denominators^-1 (basis.py:101-106) */
+  const double* gauss_nodes;  /* 2p+2 */
+  const double* gauss_weights;/* 2p+2 */
+  const double* mass_inv;     /* (p+1)^2 row-major */
+} SldgBasis;
+
+/* ---------------------------------------------------------------- v-sweep */
+typedef struct sldg_vplan sldg_vplan;
+
+typedef struct SldgVPlanDesc {
+  SldgBasis basis;
+  int32_t dim;                /* 1 or 3 */
+  int32_t direction;          /* sweep axis, < dim */
+  int32_t n_levels;           /* max level + 1 */
+  double radius;              /* domain half width R */
+  double base_width;          /* 2R / n_base (VelocityMesh.base_width) */
+  int64_t n_cells;            /* mesh cells; n_dofs = n_cells*(p+1)^dim */
+  int64_t n_pencils;          /* pencils in PLAN ORDER: groups in plan order, pencils of a group in order */
+  const int64_t* pencil_offsets;  /* n_pencils+1 CSR offsets into the entry arrays */
+  const int64_t* pencil_group;    /* n_pencils: group index (write-back summation order) */
+  const int64_t* cell_ids;        /* entries */
+  const double* lowers;           /* entries: sweep-axis lower coordinate */
+  const double* widths;           /* entries: sweep-axis width */
+  const int64_t* levels;          /* entries */
+  const uint8_t* conforming;      /* entries: +-2 same-level flag (classify_conforming) */
+  const double* weights;          /* entries: 1/n_c */
+} SldgVPlanDesc;
+
+int sldg_vplan_create(const SldgVPlanDesc* desc, sldg_vplan** out);
+int sldg_vplan_destroy(sldg_vplan* plan);
+/* bytes of device scratch sldg_advect_v needs for n_cols columns */
+int sldg_vplan_scratch_bytes(const sldg_vplan* plan, int64_t n_cols, size_t* bytes);
+/* plan statistics: [n_entries, n_acc_slots, n_targets, n_whole_fast_pencils, n_dofs] */
+int sldg_vplan_info(const sldg_vplan* plan, int64_t* info5);
+
+/* f_out[:, c] = sweep(f_in[:, c], speeds[c]) for every column; columns with
+ * speeds[c] == 0.0 are copied bit for bit.  f_in and f_out must not alias.
+ * `scratch` is sldg_vplan_scratch_bytes() bytes of device memory. */
+int sldg_advect_v(const sldg_vplan* plan, const double* f_in, double* f_out, int64_t ld,
+                  int64_t n_cols, const double* speeds, double dt, int32_t bc,
+                  int32_t force_slow, void* scratch, void* stream);
+
+/* Per-column level matrices (debug / API mirror of precompute_level_matrices):
+ * n_shift[l*n_cols+c], frac[l*n_cols+c], mats[((l*2+ab)*o*o + k)*n_cols + c]. */
+int sldg_level_matrices(const sldg_vplan* plan, const double* speeds, int64_t n_cols, double dt,
+                        int64_t* n_shift, double* frac, double* mats, void* stream);
+
+/* Overlap pair for arbitrary fractional shifts (overlap_pair, sldg1d.py:82-100):
+ * fracs[n] device -> A[n*o*o], B[n*o*o] device (row-major per pair). */
+int sldg_overlap_pairs(const SldgBasis* basis, const double* fracs, int64_t n, double* A,
+                       double* B, void* stream);
+
+/* ---------------------------------------------------------------- x side */
+typedef struct sldg_xplan sldg_xplan;
+
+typedef struct SldgXPlanDesc {
+  SldgBasis basis;            /* degree_x basis */
+  int64_t n_cells;            /* global x cells (periodic) */
+  double h;                   /* x cell width */
+  double dt;                  /* shift time (dt/2 for a Strang half step) */
+  int64_t n_rows;             /* velocity DOFs */
+  int64_t n_speeds;           /* unique speeds (np.unique order) */
+  const double* speeds;       /* n_speeds unique speeds (host) */
+  const int32_t* row_speed;   /* n_rows: index into speeds (host) */
+} SldgXPlanDesc;
+
+int sldg_xplan_create(const SldgXPlanDesc* desc, sldg_xplan** out);
+int sldg_xplan_destroy(sldg_xplan* plan);
+/* max |n_shift| and max n_shift+1 over rows: halo cells needed [left, right] */
+int sldg_xplan_halo(const sldg_xplan* plan, int64_t* left_right);
+
+/* Periodic full-row update of rows [0, n_rows): f_out = X(f_in); rows with a
+ * zero shift are copied bit for bit.  f_in/f_out must not alias. */
+int sldg_advect_x(const sldg_xplan* plan, const double* f_in, double* f_out, int64_t ld,
+                  void* stream);
+
+/* Sharded update: f_in holds, per row, halo_l + n_local + halo_r cells starting
+ * at global cell (cell0 - halo_l) (ld_in elements per row); f_out gets n_local
+ * cells (ld_out).  Requires halo_l/halo_r >= sldg_xplan_halo(). */
+int sldg_advect_x_slab(const sldg_xplan* plan, const double* f_in, int64_t ld_in,
+                       int64_t halo_l, int64_t halo_r, int64_t n_local, double* f_out,
+                       int64_t ld_out, void* stream);
+
+/* rho[c] = sum_r w[r] f[r, c]  (deterministic two-stage column reduction).
+ * scratch: sldg_rho_scratch_bytes(). */
+int sldg_rho_scratch_bytes(int64_t n_rows, int64_t n_cols, size_t* bytes);
+int sldg_rho(const double* f, int64_t ld, int64_t n_rows, int64_t n_cols, const double* w,
+             double* rho, void* scratch, void* stream);
+
+/* (m0, m1, m2) = sum_r w_r {1, v0_r, v2_r} (sum_c f[r,c] xw[c])  -> out3 (device). */
+int sldg_moments_scratch_bytes(int64_t n_rows, size_t* bytes);
+int sldg_moments(const double* f, int64_t ld, int64_t n_rows, int64_t n_cols, const double* w,
+                 const double* v0, const double* v2, const double* xw, double* out3,
+                 void* scratch, void* stream);
+
+/* ---------------------------------------------------------------- Poisson */
+typedef struct sldg_poisson sldg_poisson;
+
+typedef struct SldgPoissonDesc {
+  int32_t degree;             /* p_x */
+  int64_t n_cells;            /* x cells */
+  double h, length;
+  const double* dof_weights;  /* n_cells*(p+1) GLL quadrature weights */
+  const double* diff;         /* (p+1)^2 differentiation matrix */
+  const double* green;        /* n_nodes^2: (augmented matrix)^-1 leading block, row-major */
+} SldgPoissonDesc;
+
+int sldg_poisson_create(const SldgPoissonDesc* desc, sldg_poisson** out);
+int sldg_poisson_destroy(sldg_poisson* p);
+/* rho (n_cells*(p+1)) -> phi (n_nodes; NULL = internal) and E (n_cells*(p+1); NULL = skip). */
+int sldg_poisson_solve(const sldg_poisson* p, const double* rho, double* phi, double* e,
+                       void* stream);
+/* E = -phi' at the DG nodes from a nodal FE potential (electric_field, xfield.py:170-179). */
+int sldg_poisson_efield(const sldg_poisson* p, const double* phi, double* e, void* stream);
+/* out2 = [max|E|, 0.5 * w.E^2]  (driver.py:220-229, xfield.py:192-195) */
+int sldg_field_diag(const sldg_poisson* p, const double* e, double* out2, void* stream);
+
+/* ---------------------------------------------------------------- misc */
+const char* sldg_last_error(void);
+int sldg_version(void);
+/* number of kernel launches enqueued by this library since load (for bench) */
+int64_t sldg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLDG_CAPI_H */

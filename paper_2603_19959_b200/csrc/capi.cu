@@ -1,0 +1,100 @@
+// capi.cu -- error plumbing, basis upload and small utility entry points.
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "sldg_common.cuh"
+
+namespace sldg {
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  return SLDG_ERR_CUDA;
+}
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+bool make_dev_basis(const SldgBasis& b, DevBasis* out, std::string* err) {
+  if (b.degree < 1 || b.degree > SLDG_MAX_DEGREE) {
+    *err = "degree " + std::to_string(b.degree) + " not compiled (1.." +
+           std::to_string(SLDG_MAX_DEGREE) + ")";
+    return false;
+  }
+  if (!b.nodes || !b.inv_denoms || !b.gauss_nodes || !b.gauss_weights || !b.mass_inv) {
+    *err = "basis arrays must be non-null";
+    return false;
+  }
+  DevBasis d{};
+  d.p = b.degree;
+  d.o = b.degree + 1;
+  d.nq = 2 * b.degree + 2;
+  for (int i = 0; i < d.o; ++i) {
+    d.nodes[i] = b.nodes[i];
+    d.inv_denoms[i] = b.inv_denoms[i];
+  }
+  for (int q = 0; q < d.nq; ++q) {
+    d.gq[q] = b.gauss_nodes[q];
+    d.gw[q] = b.gauss_weights[q];
+  }
+  for (int k = 0; k < d.o * d.o; ++k) d.minv[k] = b.mass_inv[k];
+  *out = d;
+  return true;
+}
+
+template <int O>
+__global__ void k_overlap_pairs(DevBasis b, const double* __restrict__ fracs, long long n,
+                                double* __restrict__ A, double* __restrict__ B) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double a[O * O], bb[O * O];
+  overlap_pair<O>(b, fracs[i], a, bb);
+#pragma unroll
+  for (int k = 0; k < O * O; ++k) {
+    A[i * O * O + k] = a[k];
+    B[i * O * O + k] = bb[k];
+  }
+}
+
+}  // namespace sldg
+
+using namespace sldg;
+
+extern "C" {
+
+const char* sldg_last_error(void) { return g_last_error.c_str(); }
+
+int sldg_version(void) { return 10000; }
+
+int64_t sldg_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int sldg_overlap_pairs(const SldgBasis* basis, const double* fracs, int64_t n, double* A,
+                       double* B, void* stream) {
+  DevBasis b;
+  std::string err;
+  if (!basis || !make_dev_basis(*basis, &b, &err)) {
+    set_error(basis ? err : "null basis");
+    return SLDG_ERR_ARG;
+  }
+  if (n <= 0) return SLDG_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int threads = 128;
+  int blocks = (int)((n + threads - 1) / threads);
+  switch (b.o) {
+#define CASE(O) \
+  case O: k_overlap_pairs<O><<<blocks, threads, 0, s>>>(b, fracs, n, A, B); break;
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+#undef CASE
+    default:
+      set_error("unsupported degree");
+      return SLDG_ERR_UNSUPPORTED;
+  }
+  SLDG_LAUNCH_CHECK("k_overlap_pairs");
+  return SLDG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,954 @@
+// vsweep.cu -- hybrid fast/slow SLDG v-sweep with deterministic weighted write-back.
+//
+// Replaces vsweep.advect_velocity (vsweep.py:413-441) and everything below it:
+// precompute_level_matrices (47-61), sweep_pencil (173-246: whole-pencil fast
+// path 197-200, per-cell fast path 205-219, slow path 221-245) and the
+// weighted write-back (249-272, inline 403-409).
+//
+// Data layout in HBM (the reference layout, driver.py:132-136): f[iv, ix] fp64,
+// row iv = cell*(p+1)^dim + local DOF, x fastest, leading dimension ld.  For
+// the sweep direction d, one pencil entry (pencil q, cell s) owns all
+// (p+1)^(dim-1) lines of its cell; line t, node i is local row
+//   line_off(t) + i * (p+1)^d.
+// For d = 0 a cell's (p+1)^dim rows are contiguous, so one pencil entry is one
+// contiguous (p+1)^dim x n_cols block.
+//
+// Kernels:
+//   k_level_mats      per (level, column): n_shift, alpha, A, B     (prologue)
+//   k_sweep_walk      whole-pencil-fast pencils: a CTA walks one pencil over
+//                     an x tile, streaming each cell once from HBM through a
+//                     shared-memory ring (cp.async), 16 B/DOF
+//   k_sweep_generic   every other entry: per-cell fast path with the O(1)
+//                     same-level-run check, or the slow path (generalized
+//                     overlap by on-the-fly Gauss quadrature)
+//   k_writeback       weighted targets: f_in + sum_g sum_k w (r_k - f_in) in the
+//                     reference's summation order (no atomics)
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "sldg_common.cuh"
+
+namespace sldg {
+
+struct VPlanDev {
+  const long long* p_off;     // pencil -> first entry
+  const int* p_n;             // pencil -> n cells
+  const unsigned char* p_fast;// whole-pencil fast flag
+  const int* e_pencil;        // entry -> pencil
+  const long long* e_row0;    // entry -> cell_id * n_local
+  const double* e_lower;
+  const double* e_width;
+  const int* e_level;
+  const unsigned char* e_conf;
+  const int* e_runs;          // 4 per entry: circular left/right, linear left/right
+  const int* e_slot;          // -1 = direct store, else scratch slot
+  const long long* t_row0;    // target -> first row
+  const long long* t_off;     // target -> first contribution
+  const int* c_slot;
+  const int* c_group;
+  const double* c_weight;
+  const long long* walk_pencils;  // whole-fast pencils, for k_sweep_walk
+  const long long* gen_entries;   // entries handled by k_sweep_generic when walk is used
+  long long n_entries, n_targets, n_walk, n_gen;
+  int stride_d, stride_t0, stride_t1;
+  int n_levels;
+  double radius, base_width;
+};
+
+}  // namespace sldg
+
+struct sldg_vplan {
+  sldg::DevBasis basis;
+  sldg::VPlanDev dev;
+  int dim, direction, o, n_lines, n_local;
+  long long n_cells, n_pencils, n_entries, n_slots, n_targets, n_walk, n_gen, n_dofs;
+  int max_pencil_cells;
+  void* block;
+};
+
+namespace sldg {
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+template <int O>
+__global__ void k_level_mats(DevBasis b, const double* __restrict__ speeds, long long n_cols,
+                             double dt, double base_width, int n_levels,
+                             long long* __restrict__ lm_ns, double* __restrict__ lm_frac,
+                             double* __restrict__ lm_mats) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= n_cols * n_levels) return;
+  int lev = (int)(idx / n_cols);
+  long long c = idx - (long long)lev * n_cols;
+  double width = base_width / (double)(1LL << lev);   // exact: power-of-two divisor
+  long long ns;
+  double a;
+  split_shift(speeds[c], dt, width, &ns, &a);
+  double A[O * O], B[O * O];
+  overlap_pair<O>(b, a, A, B);
+  lm_ns[idx] = ns;
+  if (lm_frac) lm_frac[idx] = a;
+#pragma unroll
+  for (int k = 0; k < O * O; ++k) {
+    lm_mats[((long long)(lev * 2 + 0) * O * O + k) * n_cols + c] = A[k];
+    lm_mats[((long long)(lev * 2 + 1) * O * O + k) * n_cols + c] = B[k];
+  }
+}
+
+template <int O>
+__device__ __forceinline__ void load_pair(const double* __restrict__ lm_mats, int lev,
+                                          long long n_cols, long long c, double* A, double* B) {
+#pragma unroll
+  for (int k = 0; k < O * O; ++k) {
+    A[k] = __ldg(lm_mats + ((long long)(lev * 2 + 0) * O * O + k) * n_cols + c);
+    B[k] = __ldg(lm_mats + ((long long)(lev * 2 + 1) * O * O + k) * n_cols + c);
+  }
+}
+
+// _fast_sources_ok (vsweep.py:125-146) in O(1) from precomputed same-level runs
+__device__ __forceinline__ bool sources_ok(const int* runs, int s, long long ns, int n, int bc) {
+  long long lo = min((long long)s, s - ns - 1);
+  long long hi = max((long long)s, s - ns);
+  if (bc == SLDG_BC_PERIODIC) {
+    if (hi - lo + 1 >= n) return runs[0] >= n;   // whole pencil one level
+    return (s - lo) <= runs[0] && (hi - s) <= runs[1];
+  }
+  long long i0 = max(lo, 0LL), i1 = min(hi, (long long)n - 1);
+  return (s - i0) <= runs[2] && (i1 - s) <= runs[3];
+}
+
+template <int O, int DIM>
+struct Lines {
+  static constexpr int NL = (DIM == 3) ? O * O : 1;
+  static constexpr int NLOC = NL * O;
+  __device__ __forceinline__ static int row(const VPlanDev& P, int t, int i) {
+    if (DIM == 1) return i;
+    return (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d;
+  }
+};
+
+// out (O values) = A ua + B ub  (apply_update, sldg1d.py:124-136: src_same@A.T + src_nb@B.T)
+template <int O>
+__device__ __forceinline__ void two_cell(const double* A, const double* B, const double* ua,
+                                         const double* ub, bool va, bool vb, double* y) {
+#pragma unroll
+  for (int i = 0; i < O; ++i) {
+    double sa = 0.0, sb = 0.0;
+    if (va) {
+      sa = A[i * O] * ua[0];
+#pragma unroll
+      for (int j = 1; j < O; ++j) sa = fma(A[i * O + j], ua[j], sa);
+    }
+    if (vb) {
+      sb = B[i * O] * ub[0];
+#pragma unroll
+      for (int j = 1; j < O; ++j) sb = fma(B[i * O + j], ub[j], sb);
+    }
+    y[i] = sa + sb;
+  }
+}
+
+// generalized overlap block M^-1 (2/dw) int_{vl}^{vr} l_i(dref) l_j(sref)   (vsweep.py:77-95)
+template <int O>
+__device__ __forceinline__ void general_block(const DevBasis& b, double vl, double vr,
+                                              double dlo, double dw, double slo, double sw,
+                                              double de, double* M) {
+  constexpr int NQ = 2 * O;
+  double raw[O * O];
+#pragma unroll
+  for (int k = 0; k < O * O; ++k) raw[k] = 0.0;
+  double half = 0.5 * (vr - vl);
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    double x = vl + half * (b.gq[q] + 1.0);
+    double w = half * b.gw[q];
+    double dref = 2.0 * (x + de - dlo) / dw - 1.0;
+    double sref = 2.0 * (x - slo) / sw - 1.0;
+    double dv[O], sv[O];
+    lagrange_all<O>(b, dref, dv);
+    lagrange_all<O>(b, sref, sv);
+#pragma unroll
+    for (int i = 0; i < O; ++i) {
+      double wd = w * dv[i];
+#pragma unroll
+      for (int j = 0; j < O; ++j) raw[i * O + j] = fma(wd, sv[j], raw[i * O + j]);
+    }
+  }
+  double sc = 2.0 / dw;
+#pragma unroll
+  for (int k = 0; k < O * O; ++k) raw[k] *= sc;
+  apply_minv<O>(b, raw, M);
+}
+
+// One (entry, column): writes the entry's NLOC outputs for column c.
+template <int O, int DIM>
+__device__ __forceinline__ void sweep_entry(const VPlanDev& P, const DevBasis& b,
+                                            const double* __restrict__ fin,
+                                            double* __restrict__ fout, long long ld,
+                                            long long n_cols, long long e, long long c,
+                                            double speed, double dt, int bc, int force_slow,
+                                            const long long* __restrict__ lm_ns,
+                                            const double* __restrict__ lm_mats,
+                                            double* __restrict__ acc) {
+  using L = Lines<O, DIM>;
+  const int q = P.e_pencil[e];
+  const long long off = P.p_off[q];
+  const int n = P.p_n[q];
+  const int s = (int)(e - off);
+  const int slot = P.e_slot[e];
+  double* dst;
+  long long dstride;
+  if (slot < 0) {
+    dst = fout + P.e_row0[e] * ld + c;
+    dstride = ld;
+  } else {
+    dst = acc + (long long)slot * L::NLOC * n_cols + c;
+    dstride = n_cols;
+  }
+  const double* self = fin + P.e_row0[e] * ld + c;
+  if (speed == 0.0) {   // exact-zero speed: untouched bits (vsweep.py:429-431)
+    for (int r = 0; r < L::NLOC; ++r) dst[r * dstride] = self[r * ld];
+    return;
+  }
+  const int lev = P.e_level[e];
+  const long long ns = lm_ns[(long long)lev * n_cols + c];
+  bool fast = false;
+  if (!force_slow) {
+    if (P.p_fast[q]) fast = true;
+    else if (P.e_conf[e]) fast = sources_ok(P.e_runs + 4 * e, s, ns, n, bc);
+  }
+  if (fast) {
+    double A[O * O], B[O * O];
+    load_pair<O>(lm_mats, lev, n_cols, c, A, B);
+    long long qa = s - ns, qb = s - ns - 1;
+    bool va = true, vb = true;
+    if (bc == SLDG_BC_PERIODIC) {
+      qa = pymod(qa, n);
+      qb = pymod(qb, n);
+    } else {
+      va = (qa >= 0 && qa < n);
+      vb = (qb >= 0 && qb < n);
+    }
+    const double* pa = fin + (va ? P.e_row0[off + qa] : 0) * ld + c;
+    const double* pb = fin + (vb ? P.e_row0[off + qb] : 0) * ld + c;
+#pragma unroll 1
+    for (int t = 0; t < L::NL; ++t) {
+      double ua[O], ub[O], y[O];
+#pragma unroll
+      for (int i = 0; i < O; ++i) {
+        int r = L::row(P, t, i);
+        ua[i] = va ? pa[(long long)r * ld] : 0.0;
+        ub[i] = vb ? pb[(long long)r * ld] : 0.0;
+      }
+      two_cell<O>(A, B, ua, ub, va, vb, y);
+#pragma unroll
+      for (int i = 0; i < O; ++i) dst[(long long)L::row(P, t, i) * dstride] = y[i];
+    }
+    return;
+  }
+
+  // ---- slow path (vsweep.py:221-245) ----
+  const double disp = __dmul_rn(speed, dt);
+  const double dlo = P.e_lower[e], dw = P.e_width[e];
+  const double flo = __dsub_rn(dlo, disp);
+  const double fhi = __dadd_rn(flo, dw);
+  double pa_[2], pz_[2], pd_[2];
+  int npieces = 0;
+  const double R = P.radius;
+  if (bc == SLDG_BC_ABSORBING) {   // _foot_segments (vsweep.py:149-170)
+    double a = fmax(flo, -R), z = fmin(fhi, R);
+    if (z > a) {
+      pa_[0] = a; pz_[0] = z; pd_[0] = disp; npieces = 1;
+    }
+  } else {
+    double span = 2.0 * R;
+    double k = floor(__ddiv_rn(__dadd_rn(flo, R), span));
+    double a = __dsub_rn(flo, __dmul_rn(k, span));
+    double z = __dsub_rn(fhi, __dmul_rn(k, span));
+    if (z <= R) {
+      pa_[0] = a; pz_[0] = z; pd_[0] = __dadd_rn(disp, __dmul_rn(k, span)); npieces = 1;
+    } else {
+      pa_[0] = a; pz_[0] = R; pd_[0] = __dadd_rn(disp, __dmul_rn(k, span));
+      pa_[1] = -R; pz_[1] = __dsub_rn(z, span);
+      pd_[1] = __dadd_rn(disp, __dmul_rn(k + 1.0, span));
+      npieces = 2;
+    }
+  }
+  const double* lows = P.e_lower + off;
+  const double* wids = P.e_width + off;
+  bool first = true;
+  for (int pc = 0; pc < npieces; ++pc) {
+    const double a = pa_[pc], z = pz_[pc], de = pd_[pc];
+    int lo = 0, hi = n;           // searchsorted(uppers, a, 'right')
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (__dadd_rn(lows[mid], wids[mid]) <= a) lo = mid + 1; else hi = mid;
+    }
+    const int c0 = lo;
+    lo = 0; hi = n;               // searchsorted(lowers, z, 'left') - 1
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (lows[mid] < z) lo = mid + 1; else hi = mid;
+    }
+    const int c1 = lo - 1;
+    for (int cc = max(c0, 0); cc <= min(c1, n - 1); ++cc) {
+      const double slo = lows[cc], sw = wids[cc];
+      const double vl = fmax(a, slo), vr = fmin(z, __dadd_rn(slo, sw));
+      if (!(__dsub_rn(vr, vl) > 1e-14 * dw)) continue;    // sliver drop (vsweep.py:230)
+      double M[O * O];
+      general_block<O>(b, vl, vr, dlo, dw, slo, sw, de, M);
+      const double* src = fin + P.e_row0[off + cc] * ld + c;
+#pragma unroll 1
+      for (int t = 0; t < L::NL; ++t) {
+        double u[O];
+#pragma unroll
+        for (int i = 0; i < O; ++i) u[i] = src[(long long)L::row(P, t, i) * ld];
+#pragma unroll
+        for (int i = 0; i < O; ++i) {
+          double y = M[i * O] * u[0];
+#pragma unroll
+          for (int j = 1; j < O; ++j) y = fma(M[i * O + j], u[j], y);
+          double* d = dst + (long long)L::row(P, t, i) * dstride;
+          *d = first ? y : (*d + y);
+        }
+      }
+      first = false;
+    }
+  }
+  if (first) {   // no source overlaps (absorbed): zero
+    for (int r = 0; r < L::NLOC; ++r) dst[r * dstride] = 0.0;
+  }
+}
+
+template <int O, int DIM>
+__global__ void __launch_bounds__(128)
+k_sweep_generic(VPlanDev P, DevBasis b, const double* __restrict__ fin,
+                double* __restrict__ fout, long long ld, long long n_cols,
+                const double* __restrict__ speeds, double dt, int bc, int force_slow,
+                const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
+                double* __restrict__ acc, long long n_items, int use_list) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= n_items * n_cols) return;
+  long long item = idx / n_cols;
+  long long c = idx - item * n_cols;
+  long long e = use_list ? P.gen_entries[item] : item;
+  sweep_entry<O, DIM>(P, b, fin, fout, ld, n_cols, e, c, __ldg(speeds + c), dt, bc, force_slow,
+                      lm_ns, lm_mats, acc);
+}
+
+// ---------------------------------------------------------------------------
+// Whole-pencil fast path: one CTA = one pencil x one tile of TX columns, all
+// lines.  Cells are streamed in pencil order into a shared-memory ring with
+// cp.async (16 B, L1-bypassing); each cell of the pencil is read from HBM
+// exactly once, the wrap cells of a periodic pencil are kept resident.  Each
+// thread owns one column (matrices in registers) and a subset of lines.
+// Valid when every column of the tile has n_shift in [-1, 0] (the Landau
+// regime; checked per tile, the kernel falls back to direct loads otherwise).
+// ---------------------------------------------------------------------------
+template <int O, int DIM, int TX>
+struct WalkCfg {
+  static constexpr int NL = Lines<O, DIM>::NL;
+  static constexpr int NLOC = NL * O;
+  static constexpr int RING = 4;                 // cells resident (s-1, s, s+1, prefetch)
+  static constexpr int CELL_DBL = NLOC * TX;     // doubles per staged cell tile
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int O, int DIM, int TX>
+__global__ void __launch_bounds__(256)
+k_sweep_walk(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
+             long long ld, long long n_cols, const double* __restrict__ speeds, int bc,
+             const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
+             double* __restrict__ acc, int n_tiles) {
+  using C = WalkCfg<O, DIM, TX>;
+  extern __shared__ __align__(16) double smem[];
+  // ring slots 0..RING-1, then 2 wrap slots (first cell, last cell of the pencil)
+  double* ring = smem;
+  double* wrap0 = smem + C::RING * C::CELL_DBL;
+  double* wrapN = wrap0 + C::CELL_DBL;
+  __shared__ int s_nsmin, s_nsmax;
+
+  const long long wp = blockIdx.x / n_tiles;
+  const int tile = blockIdx.x - (int)(wp * n_tiles);
+  const long long q = P.walk_pencils[wp];
+  const long long off = P.p_off[q];
+  const int n = P.p_n[q];
+  const long long c0 = (long long)tile * TX;
+  const int tx = (int)min((long long)TX, n_cols - c0);   // columns in this tile
+  const int tid = threadIdx.x;
+  const int lev = P.e_level[off];
+
+  if (tid == 0) { s_nsmin = 1 << 30; s_nsmax = -(1 << 30); }
+  __syncthreads();
+  // thread -> (column, line phase)
+  const int col = tid % TX;
+  const int phase = tid / TX;
+  constexpr int PHASES = 256 / TX;
+  const bool colv = col < tx;
+  const long long c = c0 + col;
+  double speed = colv ? __ldg(speeds + c) : 0.0;
+  long long ns = colv ? lm_ns[(long long)lev * n_cols + c] : 0;
+  if (colv && speed != 0.0) {
+    atomicMin(&s_nsmin, (int)max(min(ns, (long long)(1 << 29)), -(long long)(1 << 29)));
+    atomicMax(&s_nsmax, (int)max(min(ns, (long long)(1 << 29)), -(long long)(1 << 29)));
+  }
+  __syncthreads();
+  const bool window_ok = (s_nsmin >= -1 && s_nsmax <= 0) || (s_nsmin > s_nsmax);
+  const bool vec_ok = ((ld & 1) == 0) && ((tx & 1) == 0) && ((c0 & 1) == 0) &&
+                      ((((unsigned long long)fin) & 15) == 0);
+
+  double A[O * O], B[O * O];
+  if (colv) load_pair<O>(lm_mats, lev, n_cols, c, A, B);
+
+  if (!window_ok || !vec_ok) {
+    // direct-load fallback for this tile (arbitrary shifts)
+    if (!colv) return;
+    for (int s = 0; s < n; ++s) {
+      const long long e = off + s;
+      const int slot = P.e_slot[e];
+      double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c
+                             : acc + (long long)slot * C::NLOC * n_cols + c;
+      const long long dstride = slot < 0 ? ld : n_cols;
+      const double* self = fin + P.e_row0[e] * ld + c;
+      if (speed == 0.0) {
+        for (int r = phase; r < C::NLOC; r += PHASES) dst[r * dstride] = self[r * ld];
+        continue;
+      }
+      long long qa = s - ns, qb = s - ns - 1;
+      bool va = true, vb = true;
+      if (bc == SLDG_BC_PERIODIC) { qa = pymod(qa, n); qb = pymod(qb, n); }
+      else { va = qa >= 0 && qa < n; vb = qb >= 0 && qb < n; }
+      const double* pa = fin + (va ? P.e_row0[off + qa] : 0) * ld + c;
+      const double* pb = fin + (vb ? P.e_row0[off + qb] : 0) * ld + c;
+      for (int t = phase; t < C::NL; t += PHASES) {
+        double ua[O], ub[O], y[O];
+#pragma unroll
+        for (int i = 0; i < O; ++i) {
+          int r = Lines<O, DIM>::row(P, t, i);
+          ua[i] = va ? pa[(long long)r * ld] : 0.0;
+          ub[i] = vb ? pb[(long long)r * ld] : 0.0;
+        }
+        two_cell<O>(A, B, ua, ub, va, vb, y);
+#pragma unroll
+        for (int i = 0; i < O; ++i) dst[(long long)Lines<O, DIM>::row(P, t, i) * dstride] = y[i];
+      }
+    }
+    return;
+  }
+
+  // ---- staged walk: cell j of the pencil lives in ring slot j % RING ----
+  // tile of one cell in smem: [local row r][col] (TX doubles per row)
+  auto stage = [&](int j, double* buf) {
+    const double* g = fin + P.e_row0[off + j] * ld + c0;
+    constexpr int V = TX / 2;                      // 16-byte chunks per row
+    const int chunks = C::NLOC * (tx / 2);
+    for (int k = tid; k < chunks; k += 256) {
+      int r = k / (tx / 2), v = k - r * (tx / 2);
+      cp_async16(buf + r * TX + 2 * v, g + (long long)r * ld + 2 * v);
+    }
+    (void)V;
+  };
+  auto slot_of = [&](int j) -> double* {
+    if (bc == SLDG_BC_PERIODIC) {
+      if (j == 0) return wrap0;
+      if (j == n - 1) return wrapN;
+    }
+    return ring + (j % C::RING) * C::CELL_DBL;
+  };
+  // prologue: wrap cells (periodic), then cells 0, 1 (ring)
+  if (bc == SLDG_BC_PERIODIC) {
+    stage(0, wrap0);
+    if (n > 1) stage(n - 1, wrapN);
+  }
+  cp_async_commit();
+  for (int j = 0; j < 2; ++j) {
+    if (j < n && !(bc == SLDG_BC_PERIODIC && (j == 0 || j == n - 1))) stage(j, slot_of(j));
+    cp_async_commit();
+  }
+  for (int s = 0; s < n; ++s) {
+    // prefetch cell s+2 (needed by s+1 when ns = -1 reads s+2)
+    const int jn = s + 2;
+    if (jn < n && !(bc == SLDG_BC_PERIODIC && (jn == 0 || jn == n - 1))) stage(jn, slot_of(jn));
+    cp_async_commit();
+    cp_async_wait<1>();       // everything up to cell s+1 landed
+    __syncthreads();
+    const long long e = off + s;
+    const int slot = P.e_slot[e];
+    if (colv) {
+      double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c
+                             : acc + (long long)slot * C::NLOC * n_cols + c;
+      const long long dstride = slot < 0 ? ld : n_cols;
+      if (speed == 0.0) {
+        const double* me = slot_of(s) + col;
+        for (int r = phase; r < C::NLOC; r += PHASES) dst[r * dstride] = me[r * TX];
+      } else {
+        long long qa = s - ns, qb = s - ns - 1;
+        bool va = true, vb = true;
+        if (bc == SLDG_BC_PERIODIC) { qa = pymod(qa, n); qb = pymod(qb, n); }
+        else { va = qa >= 0 && qa < n; vb = qb >= 0 && qb < n; }
+        const double* sa = slot_of(va ? (int)qa : s) + col;
+        const double* sb = slot_of(vb ? (int)qb : s) + col;
+        for (int t = phase; t < C::NL; t += PHASES) {
+          double ua[O], ub[O], y[O];
+#pragma unroll
+          for (int i = 0; i < O; ++i) {
+            int r = Lines<O, DIM>::row(P, t, i);
+            ua[i] = va ? sa[r * TX] : 0.0;
+            ub[i] = vb ? sb[r * TX] : 0.0;
+          }
+          two_cell<O>(A, B, ua, ub, va, vb, y);
+#pragma unroll
+          for (int i = 0; i < O; ++i)
+            dst[(long long)Lines<O, DIM>::row(P, t, i) * dstride] = y[i];
+        }
+      }
+    }
+    __syncthreads();          // ring slot of cell s-1 may be overwritten next
+  }
+  cp_async_wait<0>();
+}
+
+// weighted write-back (vsweep.py:403-409): out = ((f_in + S_g1) + S_g2) + ...,
+// S_g = sum over the group's contributions in flat order of w (r - f_in).
+template <int NLOC>
+__global__ void k_writeback(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
+                            long long ld, long long n_cols, const double* __restrict__ speeds,
+                            const double* __restrict__ acc) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  long long per_t = (long long)NLOC * n_cols;
+  if (idx >= P.n_targets * per_t) return;
+  long long t = idx / per_t;
+  long long rem = idx - t * per_t;
+  int r = (int)(rem / n_cols);
+  long long c = rem - (long long)r * n_cols;
+  long long row = P.t_row0[t] + r;
+  double fv = fin[row * ld + c];
+  if (__ldg(speeds + c) == 0.0) {
+    fout[row * ld + c] = fv;
+    return;
+  }
+  long long k0 = P.t_off[t], k1 = P.t_off[t + 1];
+  double o = fv, s = 0.0;
+  int g = P.c_group[k0];
+  for (long long k = k0; k < k1; ++k) {
+    int gk = P.c_group[k];
+    if (gk != g) {
+      o = __dadd_rn(o, s);
+      s = 0.0;
+      g = gk;
+    }
+    double rv = acc[((long long)P.c_slot[k] * NLOC + r) * n_cols + c];
+    s = __dadd_rn(s, __dmul_rn(P.c_weight[k], __dsub_rn(rv, fv)));
+  }
+  fout[row * ld + c] = __dadd_rn(o, s);
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct ScratchLayout {
+  size_t ns_off, frac_off, mats_off, acc_off, total;
+};
+
+static ScratchLayout scratch_layout(const sldg_vplan* p, long long n_cols) {
+  ScratchLayout L;
+  size_t off = 0;
+  L.ns_off = off;
+  off = align_up(off + sizeof(long long) * p->dev.n_levels * n_cols, 256);
+  L.frac_off = off;
+  off = align_up(off + sizeof(double) * p->dev.n_levels * n_cols, 256);
+  L.mats_off = off;
+  off = align_up(off + sizeof(double) * p->dev.n_levels * 2 * p->o * p->o * n_cols, 256);
+  L.acc_off = off;
+  off = align_up(off + sizeof(double) * (size_t)p->n_slots * p->n_local * n_cols, 256);
+  L.total = off;
+  return L;
+}
+
+template <int O>
+static int launch_level_mats(const sldg_vplan* p, const double* speeds, long long n_cols,
+                             double dt, long long* ns, double* frac, double* mats,
+                             cudaStream_t st) {
+  long long n = n_cols * p->dev.n_levels;
+  int threads = 128;
+  long long blocks = (n + threads - 1) / threads;
+  k_level_mats<O><<<(unsigned)blocks, threads, 0, st>>>(p->basis, speeds, n_cols, dt,
+                                                       p->dev.base_width, p->dev.n_levels, ns,
+                                                       frac, mats);
+  SLDG_LAUNCH_CHECK("k_level_mats");
+  return SLDG_OK;
+}
+
+template <int O, int DIM>
+static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, long long ld,
+                        long long n_cols, const double* speeds, double dt, int bc, int force_slow,
+                        const long long* lm_ns, const double* lm_mats, double* acc,
+                        cudaStream_t st) {
+  constexpr int NLOC = Lines<O, DIM>::NLOC;
+  constexpr int TX = 32;
+  using C = WalkCfg<O, DIM, TX>;
+  const size_t smem = sizeof(double) * (size_t)(C::RING + 2) * C::CELL_DBL;
+  const bool use_walk = !force_slow && p->n_walk > 0 && n_cols >= 2 && smem <= 200 * 1024;
+  if (use_walk) {
+    SLDG_CUDA_TRY(cudaFuncSetAttribute(k_sweep_walk<O, DIM, TX>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int n_tiles = (int)((n_cols + TX - 1) / TX);
+    long long blocks = p->n_walk * n_tiles;
+    k_sweep_walk<O, DIM, TX><<<(unsigned)blocks, 256, smem, st>>>(
+        p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, n_tiles);
+    SLDG_LAUNCH_CHECK("k_sweep_walk");
+    if (p->n_gen > 0) {
+      long long n = p->n_gen * n_cols;
+      k_sweep_generic<O, DIM><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+          p->dev, p->basis, fin, fout, ld, n_cols, speeds, dt, bc, force_slow, lm_ns, lm_mats,
+          acc, p->n_gen, 1);
+      SLDG_LAUNCH_CHECK("k_sweep_generic");
+    }
+  } else {
+    long long n = p->n_entries * n_cols;
+    k_sweep_generic<O, DIM><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+        p->dev, p->basis, fin, fout, ld, n_cols, speeds, dt, bc, force_slow, lm_ns, lm_mats, acc,
+        p->n_entries, 0);
+    SLDG_LAUNCH_CHECK("k_sweep_generic");
+  }
+  if (p->n_targets > 0) {
+    long long n = p->n_targets * NLOC * n_cols;
+    k_writeback<NLOC><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p->dev, fin, fout, ld, n_cols,
+                                                                    speeds, acc);
+    SLDG_LAUNCH_CHECK("k_writeback");
+  }
+  return SLDG_OK;
+}
+
+}  // namespace sldg
+
+using namespace sldg;
+
+extern "C" {
+
+int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
+  if (!d || !out) {
+    set_error("null argument");
+    return SLDG_ERR_ARG;
+  }
+  *out = nullptr;
+  DevBasis basis;
+  std::string err;
+  if (!make_dev_basis(d->basis, &basis, &err)) {
+    set_error(err);
+    return SLDG_ERR_ARG;
+  }
+  if (d->dim != 1 && d->dim != 3) {
+    set_error("dim must be 1 or 3");
+    return SLDG_ERR_ARG;
+  }
+  if (d->direction < 0 || d->direction >= d->dim) {
+    set_error("direction out of range");
+    return SLDG_ERR_ARG;
+  }
+  if (d->n_pencils < 1 || d->n_cells < 1 || d->n_levels < 1 || d->n_levels > 30) {
+    set_error("empty plan");
+    return SLDG_ERR_ARG;
+  }
+  const int o = basis.o;
+  const int nl = d->dim == 3 ? o * o : 1;
+  const int nloc = nl * o;
+  const long long P = d->n_pencils;
+  const long long E = d->pencil_offsets[P];
+  if (d->pencil_offsets[0] != 0 || E < 1) {
+    set_error("bad pencil offsets");
+    return SLDG_ERR_PLAN;
+  }
+  // host-side derived arrays
+  std::vector<long long> p_off(P);
+  std::vector<int> p_n(P);
+  std::vector<unsigned char> p_fast(P);
+  std::vector<int> e_pencil(E), e_level(E), e_runs(4 * E), e_slot(E, -1);
+  std::vector<long long> e_row0(E);
+  std::vector<unsigned char> e_conf(E);
+  std::vector<long long> cover(d->n_cells, 0);
+  int max_cells = 0;
+  for (long long q = 0; q < P; ++q) {
+    long long a = d->pencil_offsets[q], b = d->pencil_offsets[q + 1];
+    if (b <= a) {
+      set_error("empty pencil");
+      return SLDG_ERR_PLAN;
+    }
+    int n = (int)(b - a);
+    max_cells = std::max(max_cells, n);
+    p_off[q] = a;
+    p_n[q] = n;
+    bool allconf = true, onelev = true;
+    for (long long e = a; e < b; ++e) {
+      long long cid = d->cell_ids[e];
+      if (cid < 0 || cid >= d->n_cells) {
+        set_error("cell id out of range");
+        return SLDG_ERR_PLAN;
+      }
+      cover[cid] += 1;
+      e_pencil[e] = (int)q;
+      e_row0[e] = cid * nloc;
+      e_level[e] = (int)d->levels[e];
+      if (e_level[e] < 0 || e_level[e] >= d->n_levels) {
+        set_error("level out of range");
+        return SLDG_ERR_PLAN;
+      }
+      e_conf[e] = d->conforming[e] ? 1 : 0;
+      allconf = allconf && e_conf[e];
+      onelev = onelev && (d->levels[e] == d->levels[a]);
+    }
+    p_fast[q] = (allconf && onelev) ? 1 : 0;
+    // same-level runs: linear (absorbing) and circular (periodic)
+    for (int s = 0; s < n; ++s) {
+      long long lv = d->levels[a + s];
+      int ln = 0;
+      while (s - ln - 1 >= 0 && d->levels[a + s - ln - 1] == lv) ++ln;
+      int rn = 0;
+      while (s + rn + 1 < n && d->levels[a + s + rn + 1] == lv) ++rn;
+      int lc = 0;
+      while (lc < n && d->levels[a + ((s - lc - 1) % n + n) % n] == lv) ++lc;
+      int rc = 0;
+      while (rc < n && d->levels[a + (s + rc + 1) % n] == lv) ++rc;
+      e_runs[4 * (a + s) + 0] = lc;
+      e_runs[4 * (a + s) + 1] = rc;
+      e_runs[4 * (a + s) + 2] = ln;
+      e_runs[4 * (a + s) + 3] = rn;
+    }
+  }
+  for (long long cidx = 0; cidx < d->n_cells; ++cidx)
+    if (cover[cidx] == 0) {
+      set_error("sweep plan leaves velocity DOFs uncovered (cell " + std::to_string(cidx) + ")");
+      return SLDG_ERR_PLAN;
+    }
+  // weighted entries -> scratch slots; targets grouped by cell in entry (plan) order
+  long long n_slots = 0;
+  std::map<long long, std::vector<long long>> contrib;   // cell -> entries
+  for (long long e = 0; e < E; ++e) {
+    if (d->weights[e] != 1.0) {
+      e_slot[e] = (int)n_slots++;
+      contrib[d->cell_ids[e]].push_back(e);
+    }
+  }
+  std::vector<long long> t_row0, t_off;
+  std::vector<int> c_slot, c_group;
+  std::vector<double> c_weight;
+  t_off.push_back(0);
+  for (auto& kv : contrib) {
+    t_row0.push_back(kv.first * nloc);
+    for (long long e : kv.second) {
+      c_slot.push_back(e_slot[e]);
+      c_group.push_back((int)d->pencil_group[e_pencil[e]]);
+      c_weight.push_back(d->weights[e]);
+    }
+    t_off.push_back((long long)c_slot.size());
+  }
+  // a cell must not be both a copy target and a weighted target
+  for (long long e = 0; e < E; ++e)
+    if (d->weights[e] == 1.0 && contrib.count(d->cell_ids[e])) {
+      set_error("cell mixes unit and fractional weights");
+      return SLDG_ERR_PLAN;
+    }
+  std::vector<long long> walk, gen;
+  for (long long q = 0; q < P; ++q) {
+    if (p_fast[q]) walk.push_back(q);
+    else
+      for (long long e = p_off[q]; e < p_off[q] + p_n[q]; ++e) gen.push_back(e);
+  }
+  const long long T = (long long)t_row0.size();
+  const long long K = (long long)c_slot.size();
+
+  // one device allocation, carved
+  struct Piece {
+    const void* src;
+    size_t bytes;
+    void** dst;
+  };
+  sldg_vplan* p = new sldg_vplan();
+  std::memset(&p->dev, 0, sizeof(p->dev));
+  std::vector<Piece> pieces = {
+      {p_off.data(), sizeof(long long) * P, (void**)&p->dev.p_off},
+      {p_n.data(), sizeof(int) * P, (void**)&p->dev.p_n},
+      {p_fast.data(), (size_t)P, (void**)&p->dev.p_fast},
+      {e_pencil.data(), sizeof(int) * E, (void**)&p->dev.e_pencil},
+      {e_row0.data(), sizeof(long long) * E, (void**)&p->dev.e_row0},
+      {d->lowers, sizeof(double) * E, (void**)&p->dev.e_lower},
+      {d->widths, sizeof(double) * E, (void**)&p->dev.e_width},
+      {e_level.data(), sizeof(int) * E, (void**)&p->dev.e_level},
+      {e_conf.data(), (size_t)E, (void**)&p->dev.e_conf},
+      {e_runs.data(), sizeof(int) * 4 * E, (void**)&p->dev.e_runs},
+      {e_slot.data(), sizeof(int) * E, (void**)&p->dev.e_slot},
+      {t_row0.data(), sizeof(long long) * T, (void**)&p->dev.t_row0},
+      {t_off.data(), sizeof(long long) * (T + 1), (void**)&p->dev.t_off},
+      {c_slot.data(), sizeof(int) * K, (void**)&p->dev.c_slot},
+      {c_group.data(), sizeof(int) * K, (void**)&p->dev.c_group},
+      {c_weight.data(), sizeof(double) * K, (void**)&p->dev.c_weight},
+      {walk.data(), sizeof(long long) * walk.size(), (void**)&p->dev.walk_pencils},
+      {gen.data(), sizeof(long long) * gen.size(), (void**)&p->dev.gen_entries},
+  };
+  size_t total = 0;
+  for (auto& pc : pieces) total = align_up(total + pc.bytes, 256);
+  std::vector<unsigned char> host(total, 0);
+  size_t off = 0;
+  std::vector<size_t> offs;
+  for (auto& pc : pieces) {
+    if (pc.bytes) std::memcpy(host.data() + off, pc.src, pc.bytes);
+    offs.push_back(off);
+    off = align_up(off + pc.bytes, 256);
+  }
+  cudaError_t ce = cudaMalloc(&p->block, std::max<size_t>(total, 256));
+  if (ce != cudaSuccess) {
+    delete p;
+    return cuda_fail(ce, "cudaMalloc(vplan)");
+  }
+  ce = cudaMemcpy(p->block, host.data(), total, cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) {
+    cudaFree(p->block);
+    delete p;
+    return cuda_fail(ce, "cudaMemcpy(vplan)");
+  }
+  for (size_t i = 0; i < pieces.size(); ++i)
+    *pieces[i].dst = (unsigned char*)p->block + offs[i];
+  p->basis = basis;
+  p->dim = d->dim;
+  p->direction = d->direction;
+  p->o = o;
+  p->n_lines = nl;
+  p->n_local = nloc;
+  p->n_cells = d->n_cells;
+  p->n_pencils = P;
+  p->n_entries = E;
+  p->n_slots = n_slots;
+  p->n_targets = T;
+  p->n_walk = (long long)walk.size();
+  p->n_gen = (long long)gen.size();
+  p->n_dofs = d->n_cells * nloc;
+  p->max_pencil_cells = max_cells;
+  int pw[3] = {1, o, o * o};
+  int td[2];
+  int k = 0;
+  for (int t = 0; t < 3; ++t)
+    if (t != d->direction) td[k++] = t;
+  p->dev.stride_d = pw[d->direction];
+  p->dev.stride_t0 = d->dim == 3 ? pw[td[0]] : 0;
+  p->dev.stride_t1 = d->dim == 3 ? pw[td[1]] : 0;
+  p->dev.n_entries = E;
+  p->dev.n_targets = T;
+  p->dev.n_walk = p->n_walk;
+  p->dev.n_gen = p->n_gen;
+  p->dev.n_levels = d->n_levels;
+  p->dev.radius = d->radius;
+  p->dev.base_width = d->base_width;
+  *out = p;
+  return SLDG_OK;
+}
+
+int sldg_vplan_destroy(sldg_vplan* p) {
+  if (!p) return SLDG_OK;
+  if (p->block) cudaFree(p->block);
+  delete p;
+  return SLDG_OK;
+}
+
+int sldg_vplan_scratch_bytes(const sldg_vplan* p, int64_t n_cols, size_t* bytes) {
+  if (!p || !bytes || n_cols < 0) {
+    set_error("bad argument");
+    return SLDG_ERR_ARG;
+  }
+  *bytes = scratch_layout(p, n_cols).total;
+  return SLDG_OK;
+}
+
+int sldg_vplan_info(const sldg_vplan* p, int64_t* info) {
+  if (!p || !info) {
+    set_error("bad argument");
+    return SLDG_ERR_ARG;
+  }
+  info[0] = p->n_entries;
+  info[1] = p->n_slots;
+  info[2] = p->n_targets;
+  info[3] = p->n_walk;
+  info[4] = p->n_dofs;
+  return SLDG_OK;
+}
+
+int sldg_level_matrices(const sldg_vplan* p, const double* speeds, int64_t n_cols, double dt,
+                          int64_t* n_shift, double* frac, double* mats, void* stream) {
+  if (!p || !speeds || !n_shift || !mats || n_cols < 1 || !(dt > 0.0)) {
+    set_error("bad argument");
+    return SLDG_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (p->o) {
+#define CASE(O) \
+  case O: return launch_level_mats<O>(p, speeds, n_cols, dt, (long long*)n_shift, frac, mats, st);
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+#undef CASE
+  }
+  set_error("unsupported degree");
+  return SLDG_ERR_UNSUPPORTED;
+}
+
+int sldg_advect_v(const sldg_vplan* p, const double* fin, double* fout, int64_t ld,
+                  int64_t n_cols, const double* speeds, double dt, int32_t bc,
+                  int32_t force_slow, void* scratch, void* stream) {
+  if (!p) {
+    set_error("null plan");
+    return SLDG_ERR_ARG;
+  }
+  if (bc != SLDG_BC_PERIODIC && bc != SLDG_BC_ABSORBING) {
+    set_error("boundary mode must be 'periodic' or 'absorbing'");
+    return SLDG_ERR_ARG;
+  }
+  if (n_cols == 0) return SLDG_OK;
+  if (!fin || !fout || !speeds || n_cols < 0 || ld < n_cols || fin == fout) {
+    set_error("bad field / speeds arguments (f_in and f_out must be distinct device buffers)");
+    return SLDG_ERR_ARG;
+  }
+  if (!(dt > 0.0)) {
+    set_error("time step must be positive");
+    return SLDG_ERR_ARG;
+  }
+  ScratchLayout L = scratch_layout(p, n_cols);
+  if (!scratch) {
+    set_error("scratch buffer required");
+    return SLDG_ERR_ARG;
+  }
+  unsigned char* sb = (unsigned char*)scratch;
+  long long* lm_ns = (long long*)(sb + L.ns_off);
+  double* lm_frac = (double*)(sb + L.frac_off);
+  double* lm_mats = (double*)(sb + L.mats_off);
+  double* acc = (double*)(sb + L.acc_off);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = SLDG_ERR_UNSUPPORTED;
+  switch (p->o) {
+#define CASE(O)                                                                               \
+  case O:                                                                                     \
+    rc = launch_level_mats<O>(p, speeds, n_cols, dt, lm_ns, lm_frac, lm_mats, st);            \
+    if (rc) return rc;                                                                        \
+    if (p->dim == 3)                                                                          \
+      return launch_sweep<O, 3>(p, fin, fout, ld, n_cols, speeds, dt, bc, force_slow, lm_ns,  \
+                                lm_mats, acc, st);                                            \
+    return launch_sweep<O, 1>(p, fin, fout, ld, n_cols, speeds, dt, bc, force_slow, lm_ns,    \
+                              lm_mats, acc, st);
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+#undef CASE
+  }
+  set_error("unsupported degree");
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,646 @@
+// xfield.cu -- x-advection shift, charge density, velocity moments, 1D Poisson.
+//
+// Replaces xfield.precompute_x_matrices / advect_x (xfield.py:63-104),
+// compute_rho (107-109), PoissonSolver.rhs/solve/electric_field (148-179),
+// field_energy (192-195) and driver.moments (driver.py:139-146).
+//
+// All reductions are two-stage with a fixed partition that depends only on
+// the problem shape, so results are bitwise reproducible run to run.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sldg_common.cuh"
+
+namespace sldg {
+
+struct XPlanDev {
+  const long long* ns;     // per unique speed: integer shift
+  const unsigned char* ident;  // per unique speed: n == 0 && alpha == 0
+  const double* mats;      // per unique speed: A (o*o) then B (o*o)
+  const int* row_speed;    // per row
+};
+
+}  // namespace sldg
+
+struct sldg_xplan {
+  sldg::DevBasis basis;
+  sldg::XPlanDev dev;
+  int o;
+  long long n_cells, n_rows, n_speeds;
+  long long halo_l, halo_r;
+  double h, dt;
+  void* block;
+};
+
+struct sldg_poisson {
+  int p, o;
+  long long n_cells, n_nodes, n_dofs;
+  double h, length;
+  double* xw;      // dof weights
+  double* diff;    // o*o
+  double* green;   // n_nodes^2
+  double* work;    // b (n_nodes) + scalars
+  void* block;
+};
+
+namespace sldg {
+
+template <int O>
+__global__ void k_xmats(DevBasis b, const double* __restrict__ speeds, long long n, double dt,
+                        double h, long long* __restrict__ ns, unsigned char* __restrict__ ident,
+                        double* __restrict__ mats) {
+  long long u = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  long long n_s;
+  double a;
+  split_shift(speeds[u], dt, h, &n_s, &a);
+  double A[O * O], B[O * O];
+  overlap_pair<O>(b, a, A, B);
+  ns[u] = n_s;
+  ident[u] = (n_s == 0 && a == 0.0) ? 1 : 0;
+#pragma unroll
+  for (int k = 0; k < O * O; ++k) {
+    mats[u * 2 * O * O + k] = A[k];
+    mats[u * 2 * O * O + O * O + k] = B[k];
+  }
+}
+
+// One CTA handles ROWS rows.  The rows' input segments are staged in shared
+// memory with coalesced loads, then each thread produces output DOFs
+//   out[c*O+i] = sum_j A[i][j] u[(c-n)*O+j] + B[i][j] u[(c-n-1)*O+j]
+// with periodic wrap (full rows) or halo offsets (slabs).
+template <int O>
+__global__ void __launch_bounds__(256)
+k_advect_x(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __restrict__ fout,
+           long long ld_out, long long n_rows, int in_cells, int out_cells, int halo_l,
+           int periodic, int rows_per_cta) {
+  extern __shared__ __align__(16) double srow[];
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  const int nr = (int)min((long long)rows_per_cta, n_rows - r0);
+  const int in_len = in_cells * O, out_len = out_cells * O;
+  // stage
+  for (int k = threadIdx.x; k < nr * in_len; k += blockDim.x) {
+    int r = k / in_len, j = k - r * in_len;
+    srow[k] = fin[(r0 + r) * ld_in + j];
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nr * out_len; k += blockDim.x) {
+    int r = k / out_len, j = k - r * out_len;
+    int cell = j / O, i = j - cell * O;
+    int g = X.row_speed[r0 + r];
+    const double* u = srow + (long long)r * in_len;
+    double y;
+    if (X.ident[g]) {
+      y = u[(cell + halo_l) * O + i];
+    } else {
+      long long n = X.ns[g];
+      long long ca, cb;
+      if (periodic) {
+        ca = pymod(cell - n, in_cells);
+        cb = pymod(cell - n - 1, in_cells);
+      } else {
+        ca = cell + halo_l - n;
+        cb = ca - 1;
+      }
+      const double* A = X.mats + (long long)g * 2 * O * O;
+      const double* B = A + O * O;
+      const double* ua = u + ca * O;
+      const double* ub = u + cb * O;
+      double sa = A[i * O] * ua[0];
+      double sb = B[i * O] * ub[0];
+#pragma unroll
+      for (int jj = 1; jj < O; ++jj) {
+        sa = fma(A[i * O + jj], ua[jj], sa);
+        sb = fma(B[i * O + jj], ub[jj], sb);
+      }
+      y = sa + sb;
+    }
+    fout[(r0 + r) * ld_out + j] = y;
+  }
+}
+
+// rho stage 1: CTA (chunk, 32-column tile), 8 warps stride the chunk's rows;
+// fixed-order smem combine -> partial[chunk][c]
+__global__ void __launch_bounds__(256)
+k_rho_partial(const double* __restrict__ f, long long ld, long long n_rows, long long n_cols,
+              const double* __restrict__ w, long long chunk, double* __restrict__ partial) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const long long c = (long long)blockIdx.y * 32 + lane;
+  const long long ra = (long long)blockIdx.x * chunk;
+  const long long rb = min(ra + chunk, n_rows);
+  double s0 = 0.0, s1 = 0.0;
+  if (c < n_cols) {
+    long long r = ra + wp;
+    for (; r + 8 < rb; r += 16) {
+      s0 = fma(__ldg(w + r), __ldg(f + r * ld + c), s0);
+      s1 = fma(__ldg(w + r + 8), __ldg(f + (r + 8) * ld + c), s1);
+    }
+    for (; r < rb; r += 8) s0 = fma(__ldg(w + r), __ldg(f + r * ld + c), s0);
+  }
+  red[wp][lane] = s0 + s1;
+  __syncthreads();
+  if (wp == 0 && c < n_cols) {
+    double s = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) s += red[k][lane];
+    partial[(long long)blockIdx.x * n_cols + c] = s;
+  }
+}
+
+__global__ void k_colsum(const double* __restrict__ partial, long long n_chunks, long long n_cols,
+                         double* __restrict__ out) {
+  long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
+  double s = 0.0;
+  for (long long k = 0; k < n_chunks; ++k) s += partial[k * n_cols + c];
+  out[c] = s;
+}
+
+// moments stage 1: warp per row: col_r = sum_c f[r,c] xw[c]; per CTA fixed-order
+// sums of w_r*col_r, w_r*v0_r*col_r, w_r*v2_r*col_r
+__global__ void __launch_bounds__(256)
+k_moments_partial(const double* __restrict__ f, long long ld, long long n_rows, long long n_cols,
+                  const double* __restrict__ w, const double* __restrict__ v0,
+                  const double* __restrict__ v2, const double* __restrict__ xw, long long chunk,
+                  double* __restrict__ partial) {
+  __shared__ double red[8][3];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const long long ra = (long long)blockIdx.x * chunk;
+  const long long rb = min(ra + chunk, n_rows);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  for (long long r = ra + wp; r < rb; r += 8) {
+    double s = 0.0;
+    for (long long c = lane; c < n_cols; c += 32) s = fma(__ldg(f + r * ld + c), __ldg(xw + c), s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    double ws = __ldg(w + r) * s;
+    a0 += ws;
+    a1 = fma(__ldg(w + r) * __ldg(v0 + r), s, a1);
+    a2 = fma(__ldg(w + r) * __ldg(v2 + r), s, a2);
+  }
+  if (lane == 0) {
+    red[wp][0] = a0;
+    red[wp][1] = a1;
+    red[wp][2] = a2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (int k = 0; k < 8; ++k) s += red[k][threadIdx.x];
+    partial[blockIdx.x * 3 + threadIdx.x] = s;
+  }
+}
+
+__global__ void k_sum3(const double* __restrict__ partial, long long n, double* __restrict__ out) {
+  if (threadIdx.x < 3) {
+    double s = 0.0;
+    for (long long k = 0; k < n; ++k) s += partial[k * 3 + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+// Poisson rhs (xfield.py:148-155): rbar = (w.rho)/L; b[node] += w (rho - rbar) in
+// np.add.at order (flat DOF order).  Single CTA.
+__global__ void k_poisson_rhs(const double* __restrict__ rho, const double* __restrict__ xw,
+                              long long n_cells, int p, double length, double* __restrict__ b) {
+  __shared__ double red[1024];
+  const int o = p + 1;
+  const long long n_dofs = n_cells * o, n_nodes = n_cells * p;
+  double s = 0.0;
+  for (long long k = threadIdx.x; k < n_dofs; k += blockDim.x) s = fma(xw[k], rho[k], s);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  const double rbar = red[0] / length;
+  for (long long node = threadIdx.x; node < n_nodes; node += blockDim.x) {
+    long long cell = node / p;
+    int j = (int)(node - cell * p);
+    double v;
+    if (j == 0) {
+      // shared vertex: previous cell's last DOF (flat order first), then this cell's first;
+      // node 0: cell 0 DOF 0 comes first, the wrapped last cell's DOF p second
+      long long kprev = (cell == 0 ? n_cells - 1 : cell - 1) * o + p;
+      long long kthis = cell * o;
+      double cprev = __dmul_rn(xw[kprev], __dsub_rn(rho[kprev], rbar));
+      double cthis = __dmul_rn(xw[kthis], __dsub_rn(rho[kthis], rbar));
+      v = (cell == 0) ? __dadd_rn(cthis, cprev) : __dadd_rn(cprev, cthis);
+    } else {
+      long long k = cell * o + j;
+      v = __dmul_rn(xw[k], __dsub_rn(rho[k], rbar));
+    }
+    b[node] = v;
+  }
+}
+
+// phi = G b: warp per row, fixed lane-stride + butterfly order
+__global__ void k_gemv(const double* __restrict__ G, const double* __restrict__ b, long long n,
+                       double* __restrict__ phi) {
+  const int lane = threadIdx.x & 31;
+  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (row >= n) return;
+  double s = 0.0;
+  for (long long k = lane; k < n; k += 32) s = fma(__ldg(G + row * n + k), __ldg(b + k), s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) phi[row] = s;
+}
+
+// E = (-(2/h) phi_loc) @ D^T per element (xfield.py:170-179)
+__global__ void k_efield(const double* __restrict__ phi, const double* __restrict__ D,
+                         long long n_cells, int p, double h, double* __restrict__ e) {
+  const int o = p + 1;
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= n_cells * o) return;
+  long long cell = k / o;
+  int i = (int)(k - cell * o);
+  const long long nn = n_cells * p;
+  const double sc = -(2.0 / h);
+  double s = 0.0;
+  for (int j = 0; j < o; ++j) {
+    long long node = (cell * p + j) % nn;
+    s = fma(__dmul_rn(sc, phi[node]), D[i * o + j], s);
+  }
+  e[k] = s;
+}
+
+__global__ void k_field_diag(const double* __restrict__ e, const double* __restrict__ xw,
+                             long long n, double* __restrict__ out2) {
+  __shared__ double rm[1024], rs[1024];
+  double m = 0.0, s = 0.0;
+  for (long long k = threadIdx.x; k < n; k += blockDim.x) {
+    double v = e[k];
+    m = fmax(m, fabs(v));
+    s = fma(xw[k], v * v, s);
+  }
+  rm[threadIdx.x] = m;
+  rs[threadIdx.x] = s;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
+      rm[threadIdx.x] = fmax(rm[threadIdx.x], rm[threadIdx.x + st]);
+      rs[threadIdx.x] += rs[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out2[0] = rm[0];
+    out2[1] = 0.5 * rs[0];
+  }
+}
+
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+static long long rho_chunks(long long n_rows, long long n_cols) {
+  long long tiles = (n_cols + 31) / 32;
+  long long want = std::max<long long>(1, (148LL * 8 + tiles - 1) / tiles);
+  long long chunk = std::max<long long>(64, (n_rows + want - 1) / want);
+  return (n_rows + chunk - 1) / chunk;
+}
+
+static long long moments_chunks(long long n_rows) {
+  long long chunk = std::max<long long>(64, (n_rows + 148LL * 8 - 1) / (148LL * 8));
+  return (n_rows + chunk - 1) / chunk;
+}
+
+template <int O>
+static int launch_advect_x(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
+                           long long ld_out, int in_cells, int out_cells, int halo_l, int periodic,
+                           cudaStream_t st) {
+  const int in_len = in_cells * O;
+  // rows per CTA: stage about 24 KB of input
+  int rows = std::max(1, (int)(3072 / std::max(1, in_len)));
+  rows = std::min<long long>(rows, X->n_rows);
+  size_t smem = sizeof(double) * (size_t)rows * in_len;
+  if (smem > 200 * 1024) {
+    set_error("x row too long for shared-memory staging");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  SLDG_CUDA_TRY(cudaFuncSetAttribute(k_advect_x<O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 48 * 1024)));
+  long long blocks = (X->n_rows + rows - 1) / rows;
+  k_advect_x<O><<<(unsigned)blocks, 256, smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
+                                                     in_cells, out_cells, halo_l, periodic, rows);
+  SLDG_LAUNCH_CHECK("k_advect_x");
+  return SLDG_OK;
+}
+
+}  // namespace sldg
+
+using namespace sldg;
+
+extern "C" {
+
+int sldg_xplan_create(const SldgXPlanDesc* d, sldg_xplan** out) {
+  if (!d || !out) {
+    set_error("null argument");
+    return SLDG_ERR_ARG;
+  }
+  *out = nullptr;
+  DevBasis basis;
+  std::string err;
+  if (!make_dev_basis(d->basis, &basis, &err)) {
+    set_error(err);
+    return SLDG_ERR_ARG;
+  }
+  if (d->n_cells < 4 || !(d->h > 0.0) || !(d->dt > 0.0) || d->n_rows < 0 || d->n_speeds < 0 ||
+      (d->n_rows > 0 && (!d->row_speed || !d->speeds))) {
+    set_error("bad x plan description");
+    return SLDG_ERR_ARG;
+  }
+  for (long long r = 0; r < d->n_rows; ++r)
+    if (d->row_speed[r] < 0 || d->row_speed[r] >= d->n_speeds) {
+      set_error("row speed index out of range");
+      return SLDG_ERR_ARG;
+    }
+  const int o = basis.o;
+  const long long S = std::max<long long>(d->n_speeds, 1), R = std::max<long long>(d->n_rows, 1);
+  size_t off = 0;
+  size_t o_ns = off; off = align_up(off + sizeof(long long) * S, 256);
+  size_t o_id = off; off = align_up(off + S, 256);
+  size_t o_m = off; off = align_up(off + sizeof(double) * 2 * o * o * S, 256);
+  size_t o_rs = off; off = align_up(off + sizeof(int) * R, 256);
+  size_t o_sp = off; off = align_up(off + sizeof(double) * S, 256);
+  sldg_xplan* X = new sldg_xplan();
+  cudaError_t ce = cudaMalloc(&X->block, off);
+  if (ce != cudaSuccess) {
+    delete X;
+    return cuda_fail(ce, "cudaMalloc(xplan)");
+  }
+  unsigned char* base = (unsigned char*)X->block;
+  X->dev.ns = (long long*)(base + o_ns);
+  X->dev.ident = base + o_id;
+  X->dev.mats = (double*)(base + o_m);
+  X->dev.row_speed = (int*)(base + o_rs);
+  double* dsp = (double*)(base + o_sp);
+  if (d->n_rows > 0) {
+    ce = cudaMemcpy((void*)X->dev.row_speed, d->row_speed, sizeof(int) * d->n_rows,
+                    cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess)
+      ce = cudaMemcpy(dsp, d->speeds, sizeof(double) * d->n_speeds, cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+      cudaFree(X->block);
+      delete X;
+      return cuda_fail(ce, "cudaMemcpy(xplan)");
+    }
+  }
+  X->basis = basis;
+  X->o = o;
+  X->n_cells = d->n_cells;
+  X->n_rows = d->n_rows;
+  X->n_speeds = d->n_speeds;
+  X->h = d->h;
+  X->dt = d->dt;
+  if (d->n_speeds > 0) {
+    int threads = 128;
+    int blocks = (int)((d->n_speeds + threads - 1) / threads);
+    switch (o) {
+#define CASE(O)                                                                               \
+  case O:                                                                                     \
+    k_xmats<O><<<blocks, threads>>>(basis, dsp, d->n_speeds, d->dt, d->h, (long long*)X->dev.ns, \
+                                    (unsigned char*)X->dev.ident, (double*)X->dev.mats);      \
+    break;
+      CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+#undef CASE
+    }
+    count_launch();
+    ce = cudaDeviceSynchronize();
+    if (ce != cudaSuccess) {
+      cudaFree(X->block);
+      delete X;
+      return cuda_fail(ce, "k_xmats");
+    }
+    // halo requirement from the integer shifts
+    std::vector<long long> ns(d->n_speeds);
+    cudaMemcpy(ns.data(), X->dev.ns, sizeof(long long) * d->n_speeds, cudaMemcpyDeviceToHost);
+    std::vector<unsigned char> id(d->n_speeds);
+    cudaMemcpy(id.data(), X->dev.ident, d->n_speeds, cudaMemcpyDeviceToHost);
+    long long hl = 0, hr = 0;
+    for (long long u = 0; u < d->n_speeds; ++u) {
+      if (id[u]) continue;
+      // sources: cell - n and cell - n - 1
+      hl = std::max(hl, ns[u] + 1);
+      hr = std::max(hr, -ns[u]);
+    }
+    X->halo_l = hl;
+    X->halo_r = hr;
+  }
+  *out = X;
+  return SLDG_OK;
+}
+
+int sldg_xplan_destroy(sldg_xplan* X) {
+  if (!X) return SLDG_OK;
+  if (X->block) cudaFree(X->block);
+  delete X;
+  return SLDG_OK;
+}
+
+int sldg_xplan_halo(const sldg_xplan* X, int64_t* lr) {
+  if (!X || !lr) {
+    set_error("bad argument");
+    return SLDG_ERR_ARG;
+  }
+  lr[0] = X->halo_l;
+  lr[1] = X->halo_r;
+  return SLDG_OK;
+}
+
+int sldg_advect_x(const sldg_xplan* X, const double* fin, double* fout, int64_t ld, void* stream) {
+  if (!X || !fin || !fout || fin == fout || ld < X->n_cells * X->o) {
+    set_error("bad advect_x arguments (f_in and f_out must be distinct device buffers)");
+    return SLDG_ERR_ARG;
+  }
+  if (X->n_rows == 0) return SLDG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (X->o) {
+#define CASE(O) \
+  case O: return launch_advect_x<O>(X, fin, ld, fout, ld, (int)X->n_cells, (int)X->n_cells, 0, 1, st);
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+#undef CASE
+  }
+  set_error("unsupported degree");
+  return SLDG_ERR_UNSUPPORTED;
+}
+
+int sldg_advect_x_slab(const sldg_xplan* X, const double* fin, int64_t ld_in, int64_t halo_l,
+                       int64_t halo_r, int64_t n_local, double* fout, int64_t ld_out,
+                       void* stream) {
+  if (!X || !fin || !fout || n_local < 1 || halo_l < X->halo_l || halo_r < X->halo_r ||
+      ld_in < (halo_l + n_local + halo_r) * X->o || ld_out < n_local * X->o) {
+    set_error("bad advect_x_slab arguments (halo too narrow?)");
+    return SLDG_ERR_ARG;
+  }
+  if (X->n_rows == 0) return SLDG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int in_cells = (int)(halo_l + n_local + halo_r);
+  switch (X->o) {
+#define CASE(O)                                                                             \
+  case O:                                                                                   \
+    return launch_advect_x<O>(X, fin, ld_in, fout, ld_out, in_cells, (int)n_local, (int)halo_l, \
+                              0, st);
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+#undef CASE
+  }
+  set_error("unsupported degree");
+  return SLDG_ERR_UNSUPPORTED;
+}
+
+int sldg_rho_scratch_bytes(int64_t n_rows, int64_t n_cols, size_t* bytes) {
+  if (!bytes || n_rows < 0 || n_cols < 0) {
+    set_error("bad argument");
+    return SLDG_ERR_ARG;
+  }
+  *bytes = sizeof(double) * (size_t)std::max<long long>(1, rho_chunks(n_rows, n_cols)) *
+           std::max<long long>(n_cols, 1);
+  return SLDG_OK;
+}
+
+int sldg_rho(const double* f, int64_t ld, int64_t n_rows, int64_t n_cols, const double* w,
+             double* rho, void* scratch, void* stream) {
+  if (!f || !w || !rho || !scratch || n_rows < 1 || n_cols < 1 || ld < n_cols) {
+    set_error("bad rho arguments");
+    return SLDG_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  long long nch = rho_chunks(n_rows, n_cols);
+  long long chunk = (n_rows + nch - 1) / nch;
+  nch = (n_rows + chunk - 1) / chunk;
+  dim3 grid((unsigned)nch, (unsigned)((n_cols + 31) / 32));
+  k_rho_partial<<<grid, 256, 0, st>>>(f, ld, n_rows, n_cols, w, chunk, (double*)scratch);
+  SLDG_LAUNCH_CHECK("k_rho_partial");
+  k_colsum<<<(unsigned)((n_cols + 127) / 128), 128, 0, st>>>((double*)scratch, nch, n_cols, rho);
+  SLDG_LAUNCH_CHECK("k_colsum");
+  return SLDG_OK;
+}
+
+int sldg_moments_scratch_bytes(int64_t n_rows, size_t* bytes) {
+  if (!bytes || n_rows < 0) {
+    set_error("bad argument");
+    return SLDG_ERR_ARG;
+  }
+  *bytes = sizeof(double) * 3 * (size_t)std::max<long long>(1, moments_chunks(n_rows));
+  return SLDG_OK;
+}
+
+int sldg_moments(const double* f, int64_t ld, int64_t n_rows, int64_t n_cols, const double* w,
+                 const double* v0, const double* v2, const double* xw, double* out3,
+                 void* scratch, void* stream) {
+  if (!f || !w || !v0 || !v2 || !xw || !out3 || !scratch || n_rows < 1 || n_cols < 1 ||
+      ld < n_cols) {
+    set_error("bad moments arguments");
+    return SLDG_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  long long nch = moments_chunks(n_rows);
+  long long chunk = (n_rows + nch - 1) / nch;
+  nch = (n_rows + chunk - 1) / chunk;
+  k_moments_partial<<<(unsigned)nch, 256, 0, st>>>(f, ld, n_rows, n_cols, w, v0, v2, xw, chunk,
+                                                   (double*)scratch);
+  SLDG_LAUNCH_CHECK("k_moments_partial");
+  k_sum3<<<1, 32, 0, st>>>((double*)scratch, nch, out3);
+  SLDG_LAUNCH_CHECK("k_sum3");
+  return SLDG_OK;
+}
+
+int sldg_poisson_create(const SldgPoissonDesc* d, sldg_poisson** out) {
+  if (!d || !out || d->degree < 1 || d->degree > SLDG_MAX_DEGREE || d->n_cells < 4 ||
+      !d->dof_weights || !d->diff || !d->green || !(d->h > 0.0) || !(d->length > 0.0)) {
+    set_error("bad Poisson description");
+    return SLDG_ERR_ARG;
+  }
+  *out = nullptr;
+  sldg_poisson* P = new sldg_poisson();
+  P->p = d->degree;
+  P->o = d->degree + 1;
+  P->n_cells = d->n_cells;
+  P->n_nodes = d->n_cells * d->degree;
+  P->n_dofs = d->n_cells * P->o;
+  P->h = d->h;
+  P->length = d->length;
+  size_t off = 0;
+  size_t o_xw = off; off = align_up(off + sizeof(double) * P->n_dofs, 256);
+  size_t o_d = off; off = align_up(off + sizeof(double) * P->o * P->o, 256);
+  size_t o_g = off; off = align_up(off + sizeof(double) * P->n_nodes * P->n_nodes, 256);
+  size_t o_w = off; off = align_up(off + sizeof(double) * (2 * P->n_nodes + 8), 256);
+  cudaError_t ce = cudaMalloc(&P->block, off);
+  if (ce != cudaSuccess) {
+    delete P;
+    return cuda_fail(ce, "cudaMalloc(poisson)");
+  }
+  unsigned char* base = (unsigned char*)P->block;
+  P->xw = (double*)(base + o_xw);
+  P->diff = (double*)(base + o_d);
+  P->green = (double*)(base + o_g);
+  P->work = (double*)(base + o_w);
+  ce = cudaMemcpy(P->xw, d->dof_weights, sizeof(double) * P->n_dofs, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy(P->diff, d->diff, sizeof(double) * P->o * P->o, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy(P->green, d->green, sizeof(double) * P->n_nodes * P->n_nodes,
+                    cudaMemcpyHostToDevice);
+  if (ce != cudaSuccess) {
+    cudaFree(P->block);
+    delete P;
+    return cuda_fail(ce, "cudaMemcpy(poisson)");
+  }
+  *out = P;
+  return SLDG_OK;
+}
+
+int sldg_poisson_destroy(sldg_poisson* P) {
+  if (!P) return SLDG_OK;
+  if (P->block) cudaFree(P->block);
+  delete P;
+  return SLDG_OK;
+}
+
+int sldg_poisson_solve(const sldg_poisson* P, const double* rho, double* phi, double* e,
+                       void* stream) {
+  if (!P || !rho || (!e && !phi)) {
+    set_error("bad Poisson solve arguments");
+    return SLDG_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  double* b = P->work;
+  double* ph = phi ? phi : P->work + P->n_nodes;
+  k_poisson_rhs<<<1, 1024, 0, st>>>(rho, P->xw, P->n_cells, P->p, P->length, b);
+  SLDG_LAUNCH_CHECK("k_poisson_rhs");
+  long long threads = P->n_nodes * 32;
+  k_gemv<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(P->green, b, P->n_nodes, ph);
+  SLDG_LAUNCH_CHECK("k_gemv");
+  if (e) {
+    k_efield<<<(unsigned)((P->n_dofs + 127) / 128), 128, 0, st>>>(ph, P->diff, P->n_cells, P->p,
+                                                                  P->h, e);
+    SLDG_LAUNCH_CHECK("k_efield");
+  }
+  return SLDG_OK;
+}
+
+int sldg_poisson_efield(const sldg_poisson* P, const double* phi, double* e, void* stream) {
+  if (!P || !phi || !e) {
+    set_error("bad electric_field arguments");
+    return SLDG_ERR_ARG;
+  }
+  k_efield<<<(unsigned)((P->n_dofs + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      phi, P->diff, P->n_cells, P->p, P->h, e);
+  SLDG_LAUNCH_CHECK("k_efield");
+  return SLDG_OK;
+}
+
+int sldg_field_diag(const sldg_poisson* P, const double* e, double* out2, void* stream) {
+  if (!P || !e || !out2) {
+    set_error("bad field diag arguments");
+    return SLDG_ERR_ARG;
+  }
+  k_field_diag<<<1, 1024, 0, (cudaStream_t)stream>>>(e, P->xw, P->n_dofs, out2);
+  SLDG_LAUNCH_CHECK("k_field_diag");
+  return SLDG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,264 @@
+"""CUDA path vs the reference's golden vectors and the CPU oracle (needs a B200).
+
+Tolerances: fp64 coefficients within 1e-12 relative to max|ref| (the
+north-star bar); bitwise where the reference is bitwise (zero speeds, x
+integer shifts, determinism).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2603_19959_b200 as sv  # noqa: E402
+from oracle import sldg_oracle as so  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+TOL = 1e-12
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(DEV)
+
+
+def plan_for(dim, nb, lv, p, bc):
+    m = sv.build_mesh(dim, nb, lv, 6.0)
+    b = sv.DGBasis(p)
+    ps = sv.classify_conforming(sv.extract_pencils(m, 0), m, bc)
+    return sv.build_sweep_plan(m, ps, sv.build_permutation(b, dim), b), m, b
+
+
+def test_library_loaded_from_tree():
+    from paper_2603_19959_b200 import _capi
+    lib = _capi.lib()
+    assert lib.sldg_version() >= 10000
+    assert _capi.LIB_PATH.endswith("paper_2603_19959_b200/_lib/libsldg.so")
+
+
+def test_overlap_pairs_golden(golden):
+    g = golden("basis_1d.npz")
+    for p in range(1, 6):
+        b = sv.DGBasis(p)
+        A, B = sv.sldg1d.overlap_pairs_device(b, g[f"p{p}_fracs"])
+        np.testing.assert_allclose(A, g[f"p{p}_A"], atol=1e-13, rtol=0)
+        np.testing.assert_allclose(B, g[f"p{p}_B"], atol=1e-13, rtol=0)
+        # alpha == 0 is the exact identity pair
+        z = np.nonzero(g[f"p{p}_fracs"] == 0.0)[0]
+        assert np.array_equal(A[z[0]], np.eye(p + 1)) and not B[z[0]].any()
+
+
+def test_level_matrices_match_host_split():
+    b = sv.DGBasis(3)
+    lm = sv.precompute_level_matrices(b, 0.5, 1.0, 1.0, 2)
+    assert lm.n_shift[0] == 0 and abs(lm.frac[0] - 0.5) < 1e-15
+    assert lm.n_shift[1] == 1 and lm.frac[1] == 0.0
+    for p in range(1, 6):
+        b = sv.DGBasis(p)
+        lm = sv.precompute_level_matrices(b, 0.731, 0.1, 1.3, 3)
+        for pair in lm.pairs:
+            assert np.abs(b.weights @ (pair.same + pair.neighbor) - b.weights).max() < 1e-12
+
+
+def test_device_split_shift_bit_exact(golden):
+    """k_level_mats' decompose_shift equals Python's bit for bit (incl. the 1-ulp fold)."""
+    import ctypes as C
+
+    from paper_2603_19959_b200 import _capi
+    g = golden("basis_1d.npz")
+    plan, _, _ = plan_for(1, 4, 0, 1, "periodic")
+    for s, d, w, n, fr in zip(g["shift_speed"], g["shift_dt"], g["shift_width"],
+                              g["shift_n"], g["shift_frac"]):
+        # width of level 0 is the plan's base width; rescale speed so speed*dt/width matches
+        pl, _, _ = plan_for(1, 4, 0, 1, "periodic")
+        pl.base_width = float(w)
+        pl._dev = {}
+        sp = dev([s])
+        ns = torch.empty(1, dtype=torch.int64, device=DEV)
+        fr_d = torch.empty(1, dtype=torch.float64, device=DEV)
+        mats = torch.empty(2 * 4, dtype=torch.float64, device=DEV)
+        _capi.check(_capi.lib().sldg_level_matrices(pl.device_handle(), sp.data_ptr(), 1,
+                                                     float(d), ns.data_ptr(), fr_d.data_ptr(),
+                                                     mats.data_ptr(), None))
+        assert int(ns.item()) == int(n) and float(fr_d.item()) == float(fr)
+
+
+SWEEP_CASES = list(range(24))
+
+
+def _sweep_case(g, i):
+    k = f"s{i}"
+    dim, nb, lv, p, fs = [int(v) for v in g[f"{k}_cfg"]]
+    bc = str(g[f"{k}_bc"])
+    plan, _, _ = plan_for(dim, nb, lv, p, bc)
+    speeds = g[f"{k}_speeds"]
+    f = np.random.default_rng(int(g[f"{k}_seed"])).standard_normal((plan.n_dofs, len(speeds)))
+    return plan, f, speeds, float(g[f"{k}_dt"]), bc, bool(fs), g[f"{k}_out"]
+
+
+@pytest.mark.parametrize("case", SWEEP_CASES)
+def test_advect_velocity_golden(golden, case):
+    g = golden("sweeps.npz")
+    if case >= int(g["n_cases"]):
+        pytest.skip("no such case")
+    plan, f, speeds, dt, bc, fs, ref = _sweep_case(g, case)
+    fd = dev(f)
+    out = sv.advect_velocity(fd, speeds, dt, plan, bc=bc, force_slow=fs)
+    assert out is fd
+    got = fd.cpu().numpy()
+    assert np.abs(got - ref).max() <= TOL * np.abs(ref).max(), f"case {case}"
+    # numpy in / numpy out path gives the same bits
+    fh = f.copy()
+    sv.advect_velocity(fh, speeds, dt, plan, bc=bc, force_slow=fs)
+    assert np.array_equal(fh, got)
+
+
+@pytest.mark.parametrize("bc", ["absorbing", "periodic"])
+@pytest.mark.parametrize("dim,nb,lv,p", [(3, 4, 1, 3), (3, 4, 2, 3), (3, 3, 1, 2),
+                                          (3, 5, 2, 2), (3, 8, 0, 2), (1, 16, 0, 4),
+                                          (3, 4, 0, 5)])
+def test_advect_velocity_vs_oracle(bc, dim, nb, lv, p):
+    rng = np.random.default_rng(100 + nb * 10 + lv + p)
+    plan, m, b = plan_for(dim, nb, lv, p, bc)
+    om = so.make_mesh(dim, nb, lv, 6.0)
+    oplan = so.make_plan(om, so.mark_conforming(so.make_pencils(om, 0), bc), p)
+    ncol = 40
+    f = rng.standard_normal((plan.n_dofs, ncol))
+    speeds = rng.uniform(-1.5, 1.5, size=ncol)
+    speeds[3] = 0.0
+    speeds[5] *= 25.0
+    speeds[7] = 0.021 / 0.1 * 0.5    # Landau-sized shift
+    ref = so.advect_v(f.copy(), speeds, 0.1, oplan, bc)
+    fd = dev(f)
+    sv.advect_velocity(fd, speeds, 0.1, plan, bc=bc)
+    got = fd.cpu().numpy()
+    assert np.abs(got - ref).max() <= TOL * np.abs(ref).max()
+    assert np.array_equal(got[:, 3], f[:, 3])        # zero speed: untouched bits
+    refs = so.advect_v(f.copy(), speeds, 0.1, oplan, bc, force_slow=True)
+    fs = dev(f)
+    sv.advect_velocity(fs, speeds, 0.1, plan, bc=bc, force_slow=True)
+    assert np.abs(fs.cpu().numpy() - refs).max() <= TOL * np.abs(refs).max()
+    # hybrid == forced slow within 1e-12 (acceptance C2, vsweep.py tests 171-182)
+    assert np.abs(got - fs.cpu().numpy()).max() <= 1e-12 * max(1.0, np.abs(f).max())
+
+
+def test_advect_velocity_errors():
+    plan, _, _ = plan_for(3, 4, 1, 3, "absorbing")
+    f = torch.zeros((plan.n_dofs, 3), dtype=torch.float64, device=DEV)
+    with pytest.raises(sv.SweepError):
+        sv.advect_velocity(f, np.ones(4), 0.1, plan)
+    with pytest.raises(ValueError):
+        sv.advect_velocity(f, np.ones(3), 0.1, plan, bc="reflecting")
+    before = f.clone()
+    assert sv.advect_velocity(f, np.zeros(3), 0.1, plan) is f
+    assert torch.equal(f, before)
+
+
+def test_advect_velocity_deterministic_and_tile_invariant():
+    """Bitwise run-to-run, and a column's result is independent of the other columns."""
+    plan, _, _ = plan_for(3, 6, 1, 2, "absorbing")
+    rng = np.random.default_rng(7)
+    f = rng.standard_normal((plan.n_dofs, 96))
+    sp = rng.uniform(-2.0, 2.0, 96) * 0.1
+    a, b_ = dev(f), dev(f)
+    sv.advect_velocity(a, sp, 0.1, plan)
+    sv.advect_velocity(b_, sp, 0.1, plan)
+    assert torch.equal(a, b_)
+    sub = dev(f[:, 10:13])
+    sv.advect_velocity(sub, sp[10:13], 0.1, plan)
+    assert torch.equal(sub, a[:, 10:13])
+
+
+def test_advect_velocity_mass_periodic():
+    plan, m, b = plan_for(3, 4, 1, 3, "periodic")
+    perm = sv.build_permutation(b, 3)
+    w = sv.velocity_dof_weights(m, b, perm)
+    rng = np.random.default_rng(61)
+    f = rng.standard_normal((plan.n_dofs, 3))
+    m0 = w @ f
+    fd = dev(f)
+    sv.advect_velocity(fd, np.array([0.31, -0.9, 0.02]), 0.1, plan, bc="periodic")
+    m1 = w @ fd.cpu().numpy()
+    assert np.abs((m1 - m0) / m0).max() <= 1e-12
+
+
+def test_xside_golden(golden):
+    g = golden("xside.npz")
+    for nx in (16, 64):
+        xg = sv.XGrid(nx, 2, 4.0 * np.pi)
+        plan = sv.precompute_x_matrices(xg, g[f"nx{nx}_speeds"], 0.05)
+        fd = dev(g[f"nx{nx}_f"])
+        sv.advect_x(fd, plan)
+        got = fd.cpu().numpy()
+        np.testing.assert_allclose(got, g[f"nx{nx}_out"], atol=1e-13, rtol=0)
+        # zero-speed row untouched; integer shift row an exact roll
+        np.testing.assert_array_equal(got[-2], g[f"nx{nx}_f"][-2])
+        np.testing.assert_array_equal(
+            got[-1], np.roll(g[f"nx{nx}_f"][-1].reshape(nx, 3), 3, axis=0).ravel())
+        ps = sv.PoissonSolver(xg)
+        phi = ps.solve(dev(g[f"nx{nx}_rho"]))
+        np.testing.assert_allclose(phi.cpu().numpy(), g[f"nx{nx}_phi"], atol=1e-13, rtol=0)
+        e = ps.electric_field(phi)
+        np.testing.assert_allclose(e.cpu().numpy(), g[f"nx{nx}_E"], atol=1e-12, rtol=0)
+        r = sv.compute_rho(dev(g[f"nx{nx}_ff"]), g[f"nx{nx}_vw"])
+        np.testing.assert_allclose(r.cpu().numpy(), g[f"nx{nx}_rho_of_ff"], atol=1e-13, rtol=0)
+
+
+def test_advect_x_vs_oracle_large_shifts():
+    rng = np.random.default_rng(3)
+    for nx, p in ((16, 2), (64, 2), (32, 3), (8, 1)):
+        xg = sv.XGrid(nx, p, 4.0 * np.pi)
+        sp = np.concatenate([rng.uniform(-40, 40, 30), [0.0, 0.0, 1.0]])
+        f = rng.standard_normal((len(sp), xg.n_dofs))
+        ref = so.advect_x(f.copy(), so.x_plan(so.XGrid(nx, p, 4.0 * np.pi), sp, 0.05), nx)
+        fd = dev(f)
+        sv.advect_x(fd, sv.precompute_x_matrices(xg, sp, 0.05))
+        assert np.abs(fd.cpu().numpy() - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+SIMS = {
+    "cfg1": dict(dim=3, n_base=16, levels=0, degree=1, n_x=16, n_steps=3),
+    "cfg3": dict(dim=3, n_base=4, levels=1, degree=2, n_x=64, n_steps=5),
+    "cfg4": dict(dim=3, n_base=4, levels=2, degree=3, n_x=128, n_steps=3),
+    "q3l1p": dict(dim=3, n_base=4, levels=1, degree=3, n_x=16, n_steps=4, bc="periodic"),
+    "v1": dict(dim=1, n_base=16, levels=0, degree=2, n_x=16, n_steps=5),
+}
+
+
+@pytest.mark.parametrize("name", list(SIMS))
+def test_simulation_golden(golden, name):
+    g = golden("simulations.npz")
+    kw = dict(SIMS[name])
+    sim = sv.Simulation(sv.SimConfig(**kw))
+    recs = [sim.diagnostics(sim.field_solve())]
+    for _ in range(kw["n_steps"]):
+        recs.append(sim.step())
+    arr = np.array([[r.t, r.e_max, r.m0, r.m1, r.m2, r.e_field, r.e_total] for r in recs])
+    ref = g[f"{name}_records"]
+    np.testing.assert_allclose(arr[:, [0, 2, 4, 6]], ref[:, [0, 2, 4, 6]], rtol=1e-12)
+    assert np.abs(arr[:, 1] - ref[:, 1]).max() <= 1e-10 * ref[0, 1]
+    assert np.abs(arr[:, 3] - ref[:, 3]).max() <= 1e-12 * abs(ref[:, 2]).max()
+    f = sim.f.cpu().numpy()
+    fmax = float(g[f"{name}_fmax"])
+    got = f.ravel()[g[f"{name}_sample_idx"]]
+    assert np.abs(got - g[f"{name}_sample_val"]).max() <= TOL * fmax
+    np.testing.assert_allclose(f.sum(axis=0), g[f"{name}_colsum"], rtol=1e-11)
+
+
+def test_run_matches_step_loop():
+    cfg = sv.SimConfig(dim=3, n_base=4, levels=1, degree=2, n_x=16, n_steps=6)
+    res = sv.run(cfg)
+    sim = sv.Simulation(cfg)
+    recs = [sim.diagnostics(sim.field_solve())] + [sim.step() for _ in range(6)]
+    for a, b_ in zip(res.records, recs):
+        assert a == b_
+
+
+def test_nonfinite_aborts_with_step_index():
+    cfg = sv.SimConfig(dim=1, n_base=16, levels=0, degree=2, n_x=16, n_steps=2)
+    sim = sv.Simulation(cfg)
+    sim.f[:] = float("inf")
+    with pytest.raises(RuntimeError, match="step 0"):
+        sim.run()
