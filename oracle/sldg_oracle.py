@@ -555,13 +555,24 @@ def sweep_column(fv, speed, dt, plan: Plan, bc, force_slow=False):
     return out
 
 
-def advect_v(f, speeds, dt, plan: Plan, bc=ABSORBING, force_slow=False):
-    """Column loop; exact-zero speeds skipped (vsweep.py:413-441). In place."""
+def advect_v(f, speeds, dt, plan: Plan, bc=ABSORBING, force_slow=False, workers=1):
+    """Column loop; exact-zero speeds skipped; optional thread pool over columns like the
+    reference's `workers` (vsweep.py:413-441). In place."""
     speeds = np.asarray(speeds, dtype=float)
     assert f.shape == (plan.n_dofs, speeds.size)
-    for ix in np.nonzero(speeds != 0.0)[0]:
+
+    def one(ix):
         f[:, ix] = sweep_column(np.ascontiguousarray(f[:, ix]), speeds[ix], dt, plan, bc,
                                 force_slow)
+
+    cols = np.nonzero(speeds != 0.0)[0]
+    if workers <= 1:
+        for ix in cols:
+            one(ix)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            list(pool.map(one, cols))
     return f
 
 
@@ -598,13 +609,23 @@ def x_plan(xg: XGrid, speeds, dt):
     return groups
 
 
-def advect_x(f, groups, n_cells):
-    """Periodic x shift per row group; identity rows untouched (xfield.py:82-104)."""
-    for rows, n, a, A, B in groups:
+def advect_x(f, groups, n_cells, workers=1):
+    """Periodic x shift per row group; identity rows untouched; optional thread pool over
+    speed groups like the reference (xfield.py:82-104)."""
+    def one(grp):
+        rows, n, a, A, B = grp
         if n == 0 and a == 0.0:
-            continue
+            return
         blk = f[rows].reshape(len(rows), n_cells, -1)
         f[rows] = uniform_update(blk, n, A, B, PERIODIC).reshape(len(rows), -1)
+
+    if workers <= 1:
+        for grp in groups:
+            one(grp)
+    else:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=workers) as pool:
+            list(pool.map(one, groups))
     return f
 
 
