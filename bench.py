@@ -160,8 +160,9 @@ def run_ours(args):
     lib = _capi.lib()
 
     sampler = ClockSampler(local).start()
-    for _ in range(args.warmup):
-        sim.enqueue_step(sim._e, rec)
+    table = torch.empty((max(args.steps, args.warmup), 5), dtype=torch.float64,
+                        device=sim.f.device)
+    sim.advance(args.warmup, table[:args.warmup])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -173,14 +174,8 @@ def run_ours(args):
     launches0 = lib.sldg_launch_count()
     t_wall0 = time.perf_counter()
     ev0.record(stream)
-    for k in range(args.steps):
-        sim._advect_x()
-        sim._field(sim._e)
-        ev_v[k][0].record(stream)
-        sim._advect_v(sim._e)
-        ev_v[k][1].record(stream)
-        sim._advect_x()
-        sim._diag_into(sim._e, rec)
+    # K complete Strang steps through the pipelined path run() uses
+    sim.advance(args.steps, table[:args.steps], v_events=ev_v)
     ev1.record(stream)
     torch.cuda.synchronize()
     t_wall1 = time.perf_counter()
@@ -206,10 +201,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
     breakdown = {
-        "advect_x_half": timed(sim._advect_x),
-        "rho_poisson": timed(lambda: sim._field(sim._e)),
+        "xx_fused_moments_rho": timed(lambda: sim._xx(rec[2:5])),
+        "x_half_plain": timed(sim._advect_x),
+        "x_half_rho": timed(sim._lead_x_rho),
+        "poisson": timed(lambda: sim.poisson.solve_into(sim._rho, sim._phi, sim._e)),
         "advect_v": timed(lambda: sim._advect_v(sim._e)),
-        "diagnostics": timed(lambda: sim._diag_into(sim._e, rec)),
+        "rho_standalone": timed(lambda: sim._field(sim._e)),
+        "moments_standalone": timed(lambda: sim._diag_into(sim._e, rec)),
     }
 
     # end to end through the public API with HOST buffers: every step copies the

@@ -127,6 +127,17 @@ int sldg_xplan_halo(const sldg_xplan* plan, int64_t* left_right);
 int sldg_advect_x(const sldg_xplan* plan, const double* f_in, double* f_out, int64_t ld,
                   void* stream);
 
+/* Fused pass (csrc/xfield.cu k_xadv): f_out = X^n_apply (f_in), n_apply in {1, 2}
+ * (2 = trailing half step of step n + leading half step of step n+1, bit-identical
+ * to two sldg_advect_x calls).  If mom_out3 != NULL: (m0, m1, m2) of the state
+ * after the FIRST application (needs w, v0, v2, xw); if rho_out != NULL: rho of the
+ * final output (needs w).  scratch: sldg_xadv_scratch_bytes(). */
+int sldg_xadv_scratch_bytes(const sldg_xplan* plan, size_t* bytes);
+int sldg_advect_x_fused(const sldg_xplan* plan, const double* f_in, double* f_out, int64_t ld,
+                        int32_t n_apply, const double* w, const double* v0, const double* v2,
+                        const double* xw, double* mom_out3, double* rho_out, void* scratch,
+                        void* stream);
+
 /* Sharded update: f_in holds, per row, halo_l + n_local + halo_r cells starting
  * at global cell (cell0 - halo_l) (ld_in elements per row); f_out gets n_local
  * cells (ld_out).  Requires halo_l/halo_r >= sldg_xplan_halo(). */

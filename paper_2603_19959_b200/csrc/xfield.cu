@@ -20,6 +20,7 @@ struct XPlanDev {
   const unsigned char* ident;  // per unique speed: n == 0 && alpha == 0
   const double* mats;      // per unique speed: A (o*o) then B (o*o)
   const int* row_speed;    // per row
+  const int* nsm;          // per unique speed: n_shift mod n_cells (periodic rows)
 };
 
 }  // namespace sldg
@@ -118,6 +119,185 @@ k_advect_x(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* 
       y = sa + sb;
     }
     fout[(r0 + r) * ld_out + j] = y;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined x-advection: one warp per velocity row, rows double/triple
+// buffered in shared memory with cp.async so each warp keeps NBUF-1 rows in
+// flight while it computes.  Optional fused epilogues:
+//   NAPPLY == 2 : out = X(X(in))  -- trailing half step of step n and leading
+//                 half step of step n+1 in one pass (same arithmetic as two
+//                 separate X launches, bit for bit)
+//   MOM         : moments (m0, m1, m2) of the state after the FIRST application
+//   RHO         : rho = w . f of the final output
+// Partials are per CTA in a fixed row order (grid size depends only on the
+// problem shape), reduced by k_sum3 / k_colsum: deterministic.
+// ---------------------------------------------------------------------------
+struct XEpi {
+  const double* w;     // velocity quadrature weights (rows)
+  const double* v0;    // v_x per row
+  const double* v2;    // |v|^2 per row
+  const double* xw;    // x quadrature weights (cols)
+  double* mom_part;    // [grid][3]
+  double* rho_part;    // [grid][row_len]
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16x(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int O>
+__device__ __forceinline__ void x_row_apply(const double* __restrict__ in, double* __restrict__ out,
+                                            int n_cells, int nsm, bool ident,
+                                            const double* __restrict__ A,
+                                            const double* __restrict__ B, int lane) {
+  if (ident) {
+    for (int j = lane; j < n_cells * O; j += 32) out[j] = in[j];
+    return;
+  }
+  double a[O * O], b[O * O];
+#pragma unroll
+  for (int k = 0; k < O * O; ++k) {
+    a[k] = __ldg(A + k);
+    b[k] = __ldg(B + k);
+  }
+  for (int c = lane; c < n_cells; c += 32) {
+    int ca = c - nsm;
+    if (ca < 0) ca += n_cells;
+    int cb = ca - 1;
+    if (cb < 0) cb += n_cells;
+    double ua[O], ub[O];
+#pragma unroll
+    for (int j = 0; j < O; ++j) {
+      ua[j] = in[ca * O + j];
+      ub[j] = in[cb * O + j];
+    }
+#pragma unroll
+    for (int i = 0; i < O; ++i) {
+      double sa = a[i * O] * ua[0];
+      double sb = b[i * O] * ub[0];
+#pragma unroll
+      for (int j = 1; j < O; ++j) {
+        sa = fma(a[i * O + j], ua[j], sa);
+        sb = fma(b[i * O + j], ub[j], sb);
+      }
+      out[c * O + i] = sa + sb;
+    }
+  }
+}
+
+template <int O, int NAPPLY, bool MOM, bool RHO, bool VEC>
+__global__ void __launch_bounds__(256)
+k_xadv(XPlanDev X, const int* __restrict__ nsm_tab, const double* __restrict__ fin,
+       long long ld_in, double* __restrict__ fout, long long ld_out, long long n_rows,
+       int n_cells, XEpi epi) {
+  constexpr int NBUF = 3;
+  extern __shared__ __align__(16) double sm[];
+  const int row_len = n_cells * O;
+  const int stride = (row_len + 1) & ~1;          // 16-byte aligned per-row slots
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int per_warp = (NBUF + 1 + (NAPPLY == 2 ? 1 : 0) + (RHO ? 1 : 0)) * stride;
+  double* base = sm + (long long)warp * per_warp;
+  double* bin = base;                              // NBUF input rows
+  double* bout = base + NBUF * stride;
+  double* bmid = bout + stride;                    // used when NAPPLY == 2
+  double* racc = bout + stride * (NAPPLY == 2 ? 2 : 1);
+  __shared__ double mom_red[8][3];
+
+  const long long gw = (long long)blockIdx.x * nwarps + warp;
+  const long long tw = (long long)gridDim.x * nwarps;
+  if (RHO)
+    for (int j = lane; j < row_len; j += 32) racc[j] = 0.0;
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+
+  auto issue = [&](long long r, double* dst) {
+    const double* src = fin + r * ld_in;
+    if (VEC) {
+      for (int k = lane; k < row_len / 2; k += 32) cp_async16x(dst + 2 * k, src + 2 * k);
+    } else {
+      for (int k = lane; k < row_len; k += 32) cp_async8(dst + k, src + k);
+    }
+  };
+  // prologue: NBUF-1 rows in flight
+#pragma unroll
+  for (int p = 0; p < NBUF - 1; ++p) {
+    long long r = gw + p * tw;
+    if (r < n_rows) issue(r, bin + p * stride);
+    cp_commit();
+  }
+  int it = 0;
+  for (long long r = gw; r < n_rows; r += tw, ++it) {
+    long long rn = r + (NBUF - 1) * tw;
+    if (rn < n_rows) issue(rn, bin + ((it + NBUF - 1) % NBUF) * stride);
+    cp_commit();
+    cp_wait<NBUF - 1>();
+    __syncwarp();
+    const double* cur = bin + (it % NBUF) * stride;
+    const int g = X.row_speed[r];
+    const bool ident = X.ident[g] != 0;
+    const int nsm = nsm_tab[g];
+    const double* A = X.mats + (long long)g * 2 * O * O;
+    const double* B = A + O * O;
+    double* first = (NAPPLY == 2) ? bmid : bout;
+    x_row_apply<O>(cur, first, n_cells, nsm, ident, A, B, lane);
+    __syncwarp();
+    if (MOM) {
+      double s = 0.0;
+      for (int j = lane; j < row_len; j += 32) s = fma(first[j], __ldg(epi.xw + j), s);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      const double wr = __ldg(epi.w + r);
+      m0 += wr * s;
+      m1 = fma(wr * __ldg(epi.v0 + r), s, m1);
+      m2 = fma(wr * __ldg(epi.v2 + r), s, m2);
+    }
+    if (NAPPLY == 2) {
+      x_row_apply<O>(bmid, bout, n_cells, nsm, ident, A, B, lane);
+      __syncwarp();
+    }
+    double* dst = fout + r * ld_out;
+    if (VEC) {
+      for (int k = lane; k < row_len / 2; k += 32)
+        reinterpret_cast<double2*>(dst)[k] = reinterpret_cast<const double2*>(bout)[k];
+    } else {
+      for (int k = lane; k < row_len; k += 32) dst[k] = bout[k];
+    }
+    if (RHO) {
+      const double wr = __ldg(epi.w + r);
+      for (int j = lane; j < row_len; j += 32) racc[j] = fma(wr, bout[j], racc[j]);
+    }
+    __syncwarp();
+  }
+  cp_wait<0>();
+  // CTA-level fixed-order combine
+  if (MOM) {
+    if (lane == 0) {
+      mom_red[warp][0] = m0;
+      mom_red[warp][1] = m1;
+      mom_red[warp][2] = m2;
+    }
+  }
+  __syncthreads();
+  if (MOM && threadIdx.x < 3) {
+    double s = 0.0;
+    for (int k = 0; k < nwarps; ++k) s += mom_red[k][threadIdx.x];
+    epi.mom_part[blockIdx.x * 3 + threadIdx.x] = s;
+  }
+  if (RHO) {
+    for (int j = threadIdx.x; j < row_len; j += blockDim.x) {
+      double s = 0.0;
+      for (int k = 0; k < nwarps; ++k) s += sm[(long long)k * per_warp + (racc - base) + j];
+      epi.rho_part[(long long)blockIdx.x * row_len + j] = s;
+    }
   }
 }
 
@@ -330,6 +510,79 @@ static int launch_advect_x(const sldg_xplan* X, const double* fin, long long ld_
   return SLDG_OK;
 }
 
+struct XadvGeom {
+  int wpb, grid, stride;
+  size_t smem;
+  bool ok;
+};
+
+// Geometry depends only on the row length (never on the variant), so the
+// fused and plain passes share one row->warp->CTA partition and their
+// reductions are bitwise identical.
+static XadvGeom xadv_geom(const sldg_xplan* X, int napply, bool rho) {
+  (void)napply;
+  (void)rho;
+  XadvGeom g;
+  const int row_len = (int)(X->n_cells * X->o);
+  g.stride = (row_len + 1) & ~1;
+  const size_t per_warp = sizeof(double) * (size_t)g.stride * (3 + 1 + 1 + 1);
+  g.wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (72 * 1024) / per_warp));
+  g.smem = per_warp * g.wpb;
+  g.ok = g.smem <= 200 * 1024;
+  const int ctas_per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / g.smem));
+  long long want = (X->n_rows + g.wpb - 1) / g.wpb;
+  g.grid = (int)std::max<long long>(1, std::min<long long>(want, 148LL * ctas_per_sm));
+  return g;
+}
+
+template <int O, int NAPPLY, bool MOM, bool RHO>
+static int launch_xadv_t(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
+                         long long ld_out, const XEpi& epi, const XadvGeom& g, bool vec,
+                         cudaStream_t st) {
+  if (vec) {
+    auto k = k_xadv<O, NAPPLY, MOM, RHO, true>;
+    SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(g.smem, 48 * 1024)));
+    k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, X->dev.nsm, fin, ld_in, fout, ld_out,
+                                          X->n_rows, (int)X->n_cells, epi);
+  } else {
+    auto k = k_xadv<O, NAPPLY, MOM, RHO, false>;
+    SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(g.smem, 48 * 1024)));
+    k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, X->dev.nsm, fin, ld_in, fout, ld_out,
+                                          X->n_rows, (int)X->n_cells, epi);
+  }
+  SLDG_LAUNCH_CHECK("k_xadv");
+  return SLDG_OK;
+}
+
+template <int O>
+static int launch_xadv(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
+                       long long ld_out, int napply, bool mom, bool rho, const XEpi& epi,
+                       cudaStream_t st) {
+  XadvGeom g = xadv_geom(X, napply, rho);
+  if (!g.ok) {
+    set_error("x row too long for the pipelined x kernel");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  const int row_len = (int)(X->n_cells * O);
+  const bool vec = (row_len % 2 == 0) && (ld_in % 2 == 0) && (ld_out % 2 == 0) &&
+                   ((((unsigned long long)fin) & 15) == 0) &&
+                   ((((unsigned long long)fout) & 15) == 0);
+  int key = (napply == 2 ? 4 : 0) | (mom ? 2 : 0) | (rho ? 1 : 0);
+  switch (key) {
+    case 0: return launch_xadv_t<O, 1, false, false>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
+    case 1: return launch_xadv_t<O, 1, false, true>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
+    case 2: return launch_xadv_t<O, 1, true, false>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
+    case 3: return launch_xadv_t<O, 1, true, true>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
+    case 4: return launch_xadv_t<O, 2, false, false>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
+    case 5: return launch_xadv_t<O, 2, false, true>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
+    case 6: return launch_xadv_t<O, 2, true, false>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
+    case 7: return launch_xadv_t<O, 2, true, true>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
+  }
+  return SLDG_ERR_ARG;
+}
+
 }  // namespace sldg
 
 using namespace sldg;
@@ -366,6 +619,7 @@ int sldg_xplan_create(const SldgXPlanDesc* d, sldg_xplan** out) {
   size_t o_m = off; off = align_up(off + sizeof(double) * 2 * o * o * S, 256);
   size_t o_rs = off; off = align_up(off + sizeof(int) * R, 256);
   size_t o_sp = off; off = align_up(off + sizeof(double) * S, 256);
+  size_t o_nsm = off; off = align_up(off + sizeof(int) * S, 256);
   sldg_xplan* X = new sldg_xplan();
   cudaError_t ce = cudaMalloc(&X->block, off);
   if (ce != cudaSuccess) {
@@ -377,6 +631,7 @@ int sldg_xplan_create(const SldgXPlanDesc* d, sldg_xplan** out) {
   X->dev.ident = base + o_id;
   X->dev.mats = (double*)(base + o_m);
   X->dev.row_speed = (int*)(base + o_rs);
+  X->dev.nsm = (int*)(base + o_nsm);
   double* dsp = (double*)(base + o_sp);
   if (d->n_rows > 0) {
     ce = cudaMemcpy((void*)X->dev.row_speed, d->row_speed, sizeof(int) * d->n_rows,
@@ -429,6 +684,16 @@ int sldg_xplan_create(const SldgXPlanDesc* d, sldg_xplan** out) {
     }
     X->halo_l = hl;
     X->halo_r = hr;
+    std::vector<int> nsm(d->n_speeds);
+    for (long long u = 0; u < d->n_speeds; ++u)
+      nsm[u] = (int)(((ns[u] % d->n_cells) + d->n_cells) % d->n_cells);
+    ce = cudaMemcpy((void*)X->dev.nsm, nsm.data(), sizeof(int) * d->n_speeds,
+                    cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+      cudaFree(X->block);
+      delete X;
+      return cuda_fail(ce, "cudaMemcpy(xplan nsm)");
+    }
   }
   *out = X;
   return SLDG_OK;
@@ -458,14 +723,67 @@ int sldg_advect_x(const sldg_xplan* X, const double* fin, double* fout, int64_t 
   }
   if (X->n_rows == 0) return SLDG_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  XEpi epi{};
   switch (X->o) {
-#define CASE(O) \
-  case O: return launch_advect_x<O>(X, fin, ld, fout, ld, (int)X->n_cells, (int)X->n_cells, 0, 1, st);
+#define CASE(O)                                                                     \
+  case O:                                                                           \
+    if (xadv_geom(X, 1, false).ok) return launch_xadv<O>(X, fin, ld, fout, ld, 1, false, false, epi, st); \
+    return launch_advect_x<O>(X, fin, ld, fout, ld, (int)X->n_cells, (int)X->n_cells, 0, 1, st);
     CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
 #undef CASE
   }
   set_error("unsupported degree");
   return SLDG_ERR_UNSUPPORTED;
+}
+
+int sldg_xadv_scratch_bytes(const sldg_xplan* X, size_t* bytes) {
+  if (!X || !bytes) {
+    set_error("bad argument");
+    return SLDG_ERR_ARG;
+  }
+  XadvGeom g = xadv_geom(X, 2, true);
+  *bytes = sizeof(double) * (size_t)g.grid * (3 + X->n_cells * X->o) + 256;
+  return SLDG_OK;
+}
+
+int sldg_advect_x_fused(const sldg_xplan* X, const double* fin, double* fout, int64_t ld,
+                        int32_t n_apply, const double* w, const double* v0, const double* v2,
+                        const double* xw, double* mom_out3, double* rho_out, void* scratch,
+                        void* stream) {
+  const bool mom = mom_out3 != nullptr, rho = rho_out != nullptr;
+  if (!X || !fin || !fout || fin == fout || ld < X->n_cells * X->o ||
+      (n_apply != 1 && n_apply != 2) || (mom && (!w || !v0 || !v2 || !xw)) || (rho && !w) ||
+      ((mom || rho) && !scratch)) {
+    set_error("bad advect_x_fused arguments");
+    return SLDG_ERR_ARG;
+  }
+  if (X->n_rows == 0) return SLDG_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  XadvGeom g = xadv_geom(X, n_apply, rho);
+  XEpi epi{w, v0, v2, xw, nullptr, nullptr};
+  if (scratch) {
+    epi.mom_part = (double*)scratch;
+    epi.rho_part = (double*)scratch + 3 * (size_t)g.grid;
+  }
+  int rc = SLDG_ERR_UNSUPPORTED;
+  switch (X->o) {
+#define CASE(O) \
+  case O: rc = launch_xadv<O>(X, fin, ld, fout, ld, n_apply, mom, rho, epi, st); break;
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+#undef CASE
+  }
+  if (rc) return rc;
+  if (mom) {
+    k_sum3<<<1, 32, 0, st>>>(epi.mom_part, g.grid, mom_out3);
+    SLDG_LAUNCH_CHECK("k_sum3");
+  }
+  if (rho) {
+    const long long row_len = X->n_cells * X->o;
+    k_colsum<<<(unsigned)((row_len + 127) / 128), 128, 0, st>>>(epi.rho_part, g.grid, row_len,
+                                                                rho_out);
+    SLDG_LAUNCH_CHECK("k_colsum");
+  }
+  return SLDG_OK;
 }
 
 int sldg_advect_x_slab(const sldg_xplan* X, const double* fin, int64_t ld_in, int64_t halo_l,

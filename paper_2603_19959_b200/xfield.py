@@ -116,6 +116,30 @@ def advect_x_into(f_in, f_out, plan: XAdvectionPlan):
     return f_out
 
 
+def advect_x_fused_into(f_in, f_out, plan: XAdvectionPlan, n_apply=1, mom=None, rho=None):
+    """f_out = X^n_apply(f_in) with fused epilogues (csrc/xfield.cu k_xadv).
+
+    mom = (w, v0, v2, xw, out3): moments of the state after the first
+    application; rho = (w, out): charge density of the final state.  All
+    device tensors; enqueue only.
+    """
+    from ._device import SCRATCH, current_stream
+    lib = _capi.lib()
+    h = plan.device_handle()
+    nb = C.c_size_t()
+    _capi.check(lib.sldg_xadv_scratch_bytes(h, C.byref(nb)))
+    scratch = SCRATCH.get(("xadv", id(plan)), nb.value) if (mom or rho) else None
+    w = (mom[0] if mom else rho[0]) if (mom or rho) else None
+    _capi.check(lib.sldg_advect_x_fused(
+        h, f_in.data_ptr(), f_out.data_ptr(), f_in.stride(0), int(n_apply),
+        w.data_ptr() if w is not None else None,
+        mom[1].data_ptr() if mom else None, mom[2].data_ptr() if mom else None,
+        mom[3].data_ptr() if mom else None, mom[4].data_ptr() if mom else None,
+        rho[1].data_ptr() if rho else None,
+        scratch.data_ptr() if scratch is not None else None, current_stream()), ValueError)
+    return f_out
+
+
 def advect_x(f, plan: XAdvectionPlan, workers: int = 1):
     """Periodic SLDG x update of every velocity row, in place (xfield.py:91-104)."""
     import torch
