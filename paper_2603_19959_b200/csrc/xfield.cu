@@ -155,11 +155,16 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
+}
+
+// out = X(in) for one row held in shared memory; A/B (o x o) in shared memory.
 template <int O>
 __device__ __forceinline__ void x_row_apply(const double* __restrict__ in, double* __restrict__ out,
-                                            int n_cells, int nsm, bool ident,
-                                            const double* __restrict__ A,
-                                            const double* __restrict__ B, int lane) {
+                                            int n_cells, int nsm, bool ident, const double* A,
+                                            const double* B, int lane) {
   if (ident) {
     for (int j = lane; j < n_cells * O; j += 32) out[j] = in[j];
     return;
@@ -167,8 +172,8 @@ __device__ __forceinline__ void x_row_apply(const double* __restrict__ in, doubl
   double a[O * O], b[O * O];
 #pragma unroll
   for (int k = 0; k < O * O; ++k) {
-    a[k] = __ldg(A + k);
-    b[k] = __ldg(B + k);
+    a[k] = A[k];
+    b[k] = B[k];
   }
   for (int c = lane; c < n_cells; c += 32) {
     int ca = c - nsm;
@@ -195,70 +200,114 @@ __device__ __forceinline__ void x_row_apply(const double* __restrict__ in, doubl
   }
 }
 
+// Shared-memory layout of k_xadv (host and device agree through this struct).
+struct XadvLayout {
+  int stride;        // doubles per row slot (16-byte aligned)
+  int tab_dbl;       // speed-table doubles (0 when the table stays in global memory)
+  int shared_dbl;    // CTA-shared doubles: table + x weights + nsm/ident
+  int per_warp_dbl;  // per-warp doubles
+  __host__ __device__ static constexpr int nbuf() { return 3; }
+  __host__ __device__ static constexpr int meta() { return 4; }   // [speed idx | w | v0 | v2]
+};
+
+__host__ __device__ inline XadvLayout xadv_layout(int n_cells, int o, long long n_speeds,
+                                                  bool tab_smem) {
+  XadvLayout L;
+  const int row_len = n_cells * o;
+  L.stride = (row_len + 1) & ~1;
+  L.tab_dbl = tab_smem ? (int)(n_speeds * 2 * o * o) : 0;
+  const int small = tab_smem ? (int)((n_speeds * 5 + 7) / 8 + 1) : 0;   // nsm ints + ident bytes
+  L.shared_dbl = ((L.tab_dbl + L.stride + small) + 1) & ~1;
+  // NBUF row slots (+meta), out, mid, rho accumulator: the same for every variant so all
+  // variants share one row partition (bitwise-identical reductions)
+  L.per_warp_dbl = XadvLayout::nbuf() * (L.stride + XadvLayout::meta()) + 3 * L.stride;
+  return L;
+}
+
 template <int O, int NAPPLY, bool MOM, bool RHO, bool VEC>
-__global__ void __launch_bounds__(256)
-k_xadv(XPlanDev X, const int* __restrict__ nsm_tab, const double* __restrict__ fin,
-       long long ld_in, double* __restrict__ fout, long long ld_out, long long n_rows,
-       int n_cells, XEpi epi) {
-  constexpr int NBUF = 3;
+__global__ void __launch_bounds__(256, 2)
+k_xadv(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __restrict__ fout,
+       long long ld_out, long long n_rows, int n_cells, int n_speeds, int tab_smem, XEpi epi) {
+  constexpr int NBUF = XadvLayout::nbuf();
+  constexpr int META = XadvLayout::meta();
   extern __shared__ __align__(16) double sm[];
+  const XadvLayout L = xadv_layout(n_cells, O, n_speeds, tab_smem != 0);
   const int row_len = n_cells * O;
-  const int stride = (row_len + 1) & ~1;          // 16-byte aligned per-row slots
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int per_warp = (NBUF + 1 + (NAPPLY == 2 ? 1 : 0) + (RHO ? 1 : 0)) * stride;
-  double* base = sm + (long long)warp * per_warp;
-  double* bin = base;                              // NBUF input rows
-  double* bout = base + NBUF * stride;
-  double* bmid = bout + stride;                    // used when NAPPLY == 2
-  double* racc = bout + stride * (NAPPLY == 2 ? 2 : 1);
+  double* tab = sm;
+  double* xw_s = sm + L.tab_dbl;
+  int* nsm_s = reinterpret_cast<int*>(xw_s + L.stride);
+  unsigned char* id_s = reinterpret_cast<unsigned char*>(nsm_s + n_speeds);
+  double* wbase = sm + L.shared_dbl + (long long)warp * L.per_warp_dbl;
+  double* bout = wbase + NBUF * (L.stride + META);
+  double* bmid = bout + L.stride;
+  double* racc = bmid + L.stride;
   __shared__ double mom_red[8][3];
+
+  // CTA-shared tables: speed matrices (+shift, identity flag) and x weights
+  if (tab_smem) {
+    for (int k = threadIdx.x; k < L.tab_dbl; k += blockDim.x) tab[k] = __ldg(X.mats + k);
+    for (int k = threadIdx.x; k < n_speeds; k += blockDim.x) {
+      nsm_s[k] = __ldg(X.nsm + k);
+      id_s[k] = X.ident[k];
+    }
+  }
+  if (MOM)
+    for (int k = threadIdx.x; k < row_len; k += blockDim.x) xw_s[k] = __ldg(epi.xw + k);
+  if (RHO)
+    for (int j = lane; j < row_len; j += 32) racc[j] = 0.0;
+  __syncthreads();
 
   const long long gw = (long long)blockIdx.x * nwarps + warp;
   const long long tw = (long long)gridDim.x * nwarps;
-  if (RHO)
-    for (int j = lane; j < row_len; j += 32) racc[j] = 0.0;
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
 
-  auto issue = [&](long long r, double* dst) {
+  auto issue = [&](long long r, int slot) {
+    double* dst = wbase + slot * (L.stride + META);
     const double* src = fin + r * ld_in;
     if (VEC) {
       for (int k = lane; k < row_len / 2; k += 32) cp_async16x(dst + 2 * k, src + 2 * k);
     } else {
       for (int k = lane; k < row_len; k += 32) cp_async8(dst + k, src + k);
     }
+    double* meta = dst + L.stride;
+    if (lane == 0) cp_async4(meta, X.row_speed + r);
+    if ((MOM || RHO) && lane == 1) cp_async8(meta + 1, epi.w + r);
+    if (MOM && lane == 2) cp_async8(meta + 2, epi.v0 + r);
+    if (MOM && lane == 3) cp_async8(meta + 3, epi.v2 + r);
   };
-  // prologue: NBUF-1 rows in flight
 #pragma unroll
   for (int p = 0; p < NBUF - 1; ++p) {
     long long r = gw + p * tw;
-    if (r < n_rows) issue(r, bin + p * stride);
+    if (r < n_rows) issue(r, p);
     cp_commit();
   }
   int it = 0;
   for (long long r = gw; r < n_rows; r += tw, ++it) {
     long long rn = r + (NBUF - 1) * tw;
-    if (rn < n_rows) issue(rn, bin + ((it + NBUF - 1) % NBUF) * stride);
+    if (rn < n_rows) issue(rn, (it + NBUF - 1) % NBUF);
     cp_commit();
     cp_wait<NBUF - 1>();
     __syncwarp();
-    const double* cur = bin + (it % NBUF) * stride;
-    const int g = X.row_speed[r];
-    const bool ident = X.ident[g] != 0;
-    const int nsm = nsm_tab[g];
-    const double* A = X.mats + (long long)g * 2 * O * O;
+    const double* cur = wbase + (it % NBUF) * (L.stride + META);
+    const double* meta = cur + L.stride;
+    const int g = *reinterpret_cast<const int*>(meta);
+    const bool ident = tab_smem ? (id_s[g] != 0) : (X.ident[g] != 0);
+    const int nsm = tab_smem ? nsm_s[g] : __ldg(X.nsm + g);
+    const double* A = (tab_smem ? tab : X.mats) + (long long)g * 2 * O * O;
     const double* B = A + O * O;
     double* first = (NAPPLY == 2) ? bmid : bout;
     x_row_apply<O>(cur, first, n_cells, nsm, ident, A, B, lane);
     __syncwarp();
     if (MOM) {
       double s = 0.0;
-      for (int j = lane; j < row_len; j += 32) s = fma(first[j], __ldg(epi.xw + j), s);
+      for (int j = lane; j < row_len; j += 32) s = fma(first[j], xw_s[j], s);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      const double wr = __ldg(epi.w + r);
+      const double wr = meta[1];
       m0 += wr * s;
-      m1 = fma(wr * __ldg(epi.v0 + r), s, m1);
-      m2 = fma(wr * __ldg(epi.v2 + r), s, m2);
+      m1 = fma(wr * meta[2], s, m1);
+      m2 = fma(wr * meta[3], s, m2);
     }
     if (NAPPLY == 2) {
       x_row_apply<O>(bmid, bout, n_cells, nsm, ident, A, B, lane);
@@ -272,19 +321,16 @@ k_xadv(XPlanDev X, const int* __restrict__ nsm_tab, const double* __restrict__ f
       for (int k = lane; k < row_len; k += 32) dst[k] = bout[k];
     }
     if (RHO) {
-      const double wr = __ldg(epi.w + r);
+      const double wr = meta[1];
       for (int j = lane; j < row_len; j += 32) racc[j] = fma(wr, bout[j], racc[j]);
     }
     __syncwarp();
   }
   cp_wait<0>();
-  // CTA-level fixed-order combine
-  if (MOM) {
-    if (lane == 0) {
-      mom_red[warp][0] = m0;
-      mom_red[warp][1] = m1;
-      mom_red[warp][2] = m2;
-    }
+  if (MOM && lane == 0) {
+    mom_red[warp][0] = m0;
+    mom_red[warp][1] = m1;
+    mom_red[warp][2] = m2;
   }
   __syncthreads();
   if (MOM && threadIdx.x < 3) {
@@ -293,9 +339,11 @@ k_xadv(XPlanDev X, const int* __restrict__ nsm_tab, const double* __restrict__ f
     epi.mom_part[blockIdx.x * 3 + threadIdx.x] = s;
   }
   if (RHO) {
+    const long long roff = racc - wbase;
     for (int j = threadIdx.x; j < row_len; j += blockDim.x) {
       double s = 0.0;
-      for (int k = 0; k < nwarps; ++k) s += sm[(long long)k * per_warp + (racc - base) + j];
+      for (int k = 0; k < nwarps; ++k)
+        s += sm[L.shared_dbl + (long long)k * L.per_warp_dbl + roff + j];
       epi.rho_part[(long long)blockIdx.x * row_len + j] = s;
     }
   }
@@ -330,13 +378,18 @@ k_rho_partial(const double* __restrict__ f, long long ld, long long n_rows, long
   }
 }
 
+// stage 2 column sum: one warp per column, lane-strided partial sums + butterfly
+// (fixed order for a fixed n_chunks)
 __global__ void k_colsum(const double* __restrict__ partial, long long n_chunks, long long n_cols,
                          double* __restrict__ out) {
-  long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   if (c >= n_cols) return;
   double s = 0.0;
-  for (long long k = 0; k < n_chunks; ++k) s += partial[k * n_cols + c];
-  out[c] = s;
+  for (long long k = lane; k < n_chunks; k += 32) s += partial[k * n_cols + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[c] = s;
 }
 
 // moments stage 1: warp per row: col_r = sum_c f[r,c] xw[c]; per CTA fixed-order
@@ -374,12 +427,15 @@ k_moments_partial(const double* __restrict__ f, long long ld, long long n_rows, 
   }
 }
 
+// stage 2 of the moments: warp w sums component w (launch with 96 threads)
 __global__ void k_sum3(const double* __restrict__ partial, long long n, double* __restrict__ out) {
-  if (threadIdx.x < 3) {
-    double s = 0.0;
-    for (long long k = 0; k < n; ++k) s += partial[k * 3 + threadIdx.x];
-    out[threadIdx.x] = s;
-  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w >= 3) return;
+  double s = 0.0;
+  for (long long k = lane; k < n; k += 32) s += partial[k * 3 + w];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[w] = s;
 }
 
 // Poisson rhs (xfield.py:148-155): rbar = (w.rho)/L; b[node] += w (rho - rbar) in
@@ -511,25 +567,36 @@ static int launch_advect_x(const sldg_xplan* X, const double* fin, long long ld_
 }
 
 struct XadvGeom {
-  int wpb, grid, stride;
+  int wpb, grid;
+  bool tab_smem;
   size_t smem;
   bool ok;
 };
 
-// Geometry depends only on the row length (never on the variant), so the
-// fused and plain passes share one row->warp->CTA partition and their
-// reductions are bitwise identical.
+// Geometry depends only on the problem shape (never on the variant or the
+// device), so every variant shares one row->warp->CTA partition and the
+// fused reductions are bitwise reproducible.
 static XadvGeom xadv_geom(const sldg_xplan* X, int napply, bool rho) {
   (void)napply;
   (void)rho;
   XadvGeom g;
-  const int row_len = (int)(X->n_cells * X->o);
-  g.stride = (row_len + 1) & ~1;
-  const size_t per_warp = sizeof(double) * (size_t)g.stride * (3 + 1 + 1 + 1);
-  g.wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (72 * 1024) / per_warp));
-  g.smem = per_warp * g.wpb;
-  g.ok = g.smem <= 200 * 1024;
-  const int ctas_per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / g.smem));
+  g.tab_smem = X->n_speeds * 2 * X->o * X->o * sizeof(double) <= 48 * 1024;
+  XadvLayout L = xadv_layout((int)X->n_cells, X->o, X->n_speeds, g.tab_smem);
+  const size_t budget = 227 * 1024 - 1024;
+  int best_w = 1, best_warps = 0;
+  for (int w = 1; w <= 8; ++w) {
+    size_t smem = sizeof(double) * ((size_t)L.shared_dbl + (size_t)w * L.per_warp_dbl);
+    if (smem > budget) break;
+    int ctas = (int)std::min<size_t>(budget / smem, 8);
+    if (ctas * w > best_warps) {
+      best_warps = ctas * w;
+      best_w = w;
+    }
+  }
+  g.wpb = best_w;
+  g.smem = sizeof(double) * ((size_t)L.shared_dbl + (size_t)g.wpb * L.per_warp_dbl);
+  g.ok = g.smem <= budget;
+  const int ctas_per_sm = g.ok ? (int)std::max<size_t>(1, std::min<size_t>(8, budget / g.smem)) : 1;
   long long want = (X->n_rows + g.wpb - 1) / g.wpb;
   g.grid = (int)std::max<long long>(1, std::min<long long>(want, 148LL * ctas_per_sm));
   return g;
@@ -543,14 +610,16 @@ static int launch_xadv_t(const sldg_xplan* X, const double* fin, long long ld_in
     auto k = k_xadv<O, NAPPLY, MOM, RHO, true>;
     SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<size_t>(g.smem, 48 * 1024)));
-    k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, X->dev.nsm, fin, ld_in, fout, ld_out,
-                                          X->n_rows, (int)X->n_cells, epi);
+    k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
+                                          (int)X->n_cells, (int)X->n_speeds, g.tab_smem ? 1 : 0,
+                                          epi);
   } else {
     auto k = k_xadv<O, NAPPLY, MOM, RHO, false>;
     SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<size_t>(g.smem, 48 * 1024)));
-    k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, X->dev.nsm, fin, ld_in, fout, ld_out,
-                                          X->n_rows, (int)X->n_cells, epi);
+    k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
+                                          (int)X->n_cells, (int)X->n_speeds, g.tab_smem ? 1 : 0,
+                                          epi);
   }
   SLDG_LAUNCH_CHECK("k_xadv");
   return SLDG_OK;
@@ -774,12 +843,12 @@ int sldg_advect_x_fused(const sldg_xplan* X, const double* fin, double* fout, in
   }
   if (rc) return rc;
   if (mom) {
-    k_sum3<<<1, 32, 0, st>>>(epi.mom_part, g.grid, mom_out3);
+    k_sum3<<<1, 96, 0, st>>>(epi.mom_part, g.grid, mom_out3);
     SLDG_LAUNCH_CHECK("k_sum3");
   }
   if (rho) {
     const long long row_len = X->n_cells * X->o;
-    k_colsum<<<(unsigned)((row_len + 127) / 128), 128, 0, st>>>(epi.rho_part, g.grid, row_len,
+    k_colsum<<<(unsigned)((row_len * 32 + 255) / 256), 256, 0, st>>>(epi.rho_part, g.grid, row_len,
                                                                 rho_out);
     SLDG_LAUNCH_CHECK("k_colsum");
   }
@@ -832,7 +901,7 @@ int sldg_rho(const double* f, int64_t ld, int64_t n_rows, int64_t n_cols, const 
   dim3 grid((unsigned)nch, (unsigned)((n_cols + 31) / 32));
   k_rho_partial<<<grid, 256, 0, st>>>(f, ld, n_rows, n_cols, w, chunk, (double*)scratch);
   SLDG_LAUNCH_CHECK("k_rho_partial");
-  k_colsum<<<(unsigned)((n_cols + 127) / 128), 128, 0, st>>>((double*)scratch, nch, n_cols, rho);
+  k_colsum<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>((double*)scratch, nch, n_cols, rho);
   SLDG_LAUNCH_CHECK("k_colsum");
   return SLDG_OK;
 }
@@ -861,7 +930,7 @@ int sldg_moments(const double* f, int64_t ld, int64_t n_rows, int64_t n_cols, co
   k_moments_partial<<<(unsigned)nch, 256, 0, st>>>(f, ld, n_rows, n_cols, w, v0, v2, xw, chunk,
                                                    (double*)scratch);
   SLDG_LAUNCH_CHECK("k_moments_partial");
-  k_sum3<<<1, 32, 0, st>>>((double*)scratch, nch, out3);
+  k_sum3<<<1, 96, 0, st>>>((double*)scratch, nch, out3);
   SLDG_LAUNCH_CHECK("k_sum3");
   return SLDG_OK;
 }
