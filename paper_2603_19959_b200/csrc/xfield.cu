@@ -122,232 +122,11 @@ k_advect_x(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Pipelined x-advection: one warp per velocity row, rows double/triple
-// buffered in shared memory with cp.async so each warp keeps NBUF-1 rows in
-// flight while it computes.  Optional fused epilogues:
-//   NAPPLY == 2 : out = X(X(in))  -- trailing half step of step n and leading
-//                 half step of step n+1 in one pass (same arithmetic as two
-//                 separate X launches, bit for bit)
-//   MOM         : moments (m0, m1, m2) of the state after the FIRST application
-//   RHO         : rho = w . f of the final output
-// Partials are per CTA in a fixed row order (grid size depends only on the
-// problem shape), reduced by k_sum3 / k_colsum: deterministic.
-// ---------------------------------------------------------------------------
-struct XEpi {
-  const double* w;     // velocity quadrature weights (rows)
-  const double* v0;    // v_x per row
-  const double* v2;    // |v|^2 per row
-  const double* xw;    // x quadrature weights (cols)
-  double* mom_part;    // [grid][3]
-  double* rho_part;    // [grid][row_len]
-};
+}  // namespace sldg
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async16x(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+#include "xadv_kernel.cuh"
 
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem));
-}
-
-// out = X(in) for one row held in shared memory; A/B (o x o) in shared memory.
-template <int O>
-__device__ __forceinline__ void x_row_apply(const double* __restrict__ in, double* __restrict__ out,
-                                            int n_cells, int nsm, bool ident, const double* A,
-                                            const double* B, int lane) {
-  if (ident) {
-    for (int j = lane; j < n_cells * O; j += 32) out[j] = in[j];
-    return;
-  }
-  double a[O * O], b[O * O];
-#pragma unroll
-  for (int k = 0; k < O * O; ++k) {
-    a[k] = A[k];
-    b[k] = B[k];
-  }
-  for (int c = lane; c < n_cells; c += 32) {
-    int ca = c - nsm;
-    if (ca < 0) ca += n_cells;
-    int cb = ca - 1;
-    if (cb < 0) cb += n_cells;
-    double ua[O], ub[O];
-#pragma unroll
-    for (int j = 0; j < O; ++j) {
-      ua[j] = in[ca * O + j];
-      ub[j] = in[cb * O + j];
-    }
-#pragma unroll
-    for (int i = 0; i < O; ++i) {
-      double sa = a[i * O] * ua[0];
-      double sb = b[i * O] * ub[0];
-#pragma unroll
-      for (int j = 1; j < O; ++j) {
-        sa = fma(a[i * O + j], ua[j], sa);
-        sb = fma(b[i * O + j], ub[j], sb);
-      }
-      out[c * O + i] = sa + sb;
-    }
-  }
-}
-
-// Shared-memory layout of k_xadv (host and device agree through this struct).
-struct XadvLayout {
-  int stride;        // doubles per row slot (16-byte aligned)
-  int tab_dbl;       // speed-table doubles (0 when the table stays in global memory)
-  int shared_dbl;    // CTA-shared doubles: table + x weights + nsm/ident
-  int per_warp_dbl;  // per-warp doubles
-  __host__ __device__ static constexpr int nbuf() { return 3; }
-  __host__ __device__ static constexpr int meta() { return 4; }   // [speed idx | w | v0 | v2]
-};
-
-__host__ __device__ inline XadvLayout xadv_layout(int n_cells, int o, long long n_speeds,
-                                                  bool tab_smem) {
-  XadvLayout L;
-  const int row_len = n_cells * o;
-  L.stride = (row_len + 1) & ~1;
-  L.tab_dbl = tab_smem ? (int)(n_speeds * 2 * o * o) : 0;
-  const int small = tab_smem ? (int)((n_speeds * 5 + 7) / 8 + 1) : 0;   // nsm ints + ident bytes
-  L.shared_dbl = ((L.tab_dbl + L.stride + small) + 1) & ~1;
-  // NBUF row slots (+meta), out, mid, rho accumulator: the same for every variant so all
-  // variants share one row partition (bitwise-identical reductions)
-  L.per_warp_dbl = XadvLayout::nbuf() * (L.stride + XadvLayout::meta()) + 3 * L.stride;
-  return L;
-}
-
-template <int O, int NAPPLY, bool MOM, bool RHO, bool VEC>
-__global__ void __launch_bounds__(256, 2)
-k_xadv(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __restrict__ fout,
-       long long ld_out, long long n_rows, int n_cells, int n_speeds, int tab_smem, XEpi epi) {
-  constexpr int NBUF = XadvLayout::nbuf();
-  constexpr int META = XadvLayout::meta();
-  extern __shared__ __align__(16) double sm[];
-  const XadvLayout L = xadv_layout(n_cells, O, n_speeds, tab_smem != 0);
-  const int row_len = n_cells * O;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  double* tab = sm;
-  double* xw_s = sm + L.tab_dbl;
-  int* nsm_s = reinterpret_cast<int*>(xw_s + L.stride);
-  unsigned char* id_s = reinterpret_cast<unsigned char*>(nsm_s + n_speeds);
-  double* wbase = sm + L.shared_dbl + (long long)warp * L.per_warp_dbl;
-  double* bout = wbase + NBUF * (L.stride + META);
-  double* bmid = bout + L.stride;
-  double* racc = bmid + L.stride;
-  __shared__ double mom_red[8][3];
-
-  // CTA-shared tables: speed matrices (+shift, identity flag) and x weights
-  if (tab_smem) {
-    for (int k = threadIdx.x; k < L.tab_dbl; k += blockDim.x) tab[k] = __ldg(X.mats + k);
-    for (int k = threadIdx.x; k < n_speeds; k += blockDim.x) {
-      nsm_s[k] = __ldg(X.nsm + k);
-      id_s[k] = X.ident[k];
-    }
-  }
-  if (MOM)
-    for (int k = threadIdx.x; k < row_len; k += blockDim.x) xw_s[k] = __ldg(epi.xw + k);
-  if (RHO)
-    for (int j = lane; j < row_len; j += 32) racc[j] = 0.0;
-  __syncthreads();
-
-  const long long gw = (long long)blockIdx.x * nwarps + warp;
-  const long long tw = (long long)gridDim.x * nwarps;
-  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-
-  auto issue = [&](long long r, int slot) {
-    double* dst = wbase + slot * (L.stride + META);
-    const double* src = fin + r * ld_in;
-    if (VEC) {
-      for (int k = lane; k < row_len / 2; k += 32) cp_async16x(dst + 2 * k, src + 2 * k);
-    } else {
-      for (int k = lane; k < row_len; k += 32) cp_async8(dst + k, src + k);
-    }
-    double* meta = dst + L.stride;
-    if (lane == 0) cp_async4(meta, X.row_speed + r);
-    if ((MOM || RHO) && lane == 1) cp_async8(meta + 1, epi.w + r);
-    if (MOM && lane == 2) cp_async8(meta + 2, epi.v0 + r);
-    if (MOM && lane == 3) cp_async8(meta + 3, epi.v2 + r);
-  };
-#pragma unroll
-  for (int p = 0; p < NBUF - 1; ++p) {
-    long long r = gw + p * tw;
-    if (r < n_rows) issue(r, p);
-    cp_commit();
-  }
-  int it = 0;
-  for (long long r = gw; r < n_rows; r += tw, ++it) {
-    long long rn = r + (NBUF - 1) * tw;
-    if (rn < n_rows) issue(rn, (it + NBUF - 1) % NBUF);
-    cp_commit();
-    cp_wait<NBUF - 1>();
-    __syncwarp();
-    const double* cur = wbase + (it % NBUF) * (L.stride + META);
-    const double* meta = cur + L.stride;
-    const int g = *reinterpret_cast<const int*>(meta);
-    const bool ident = tab_smem ? (id_s[g] != 0) : (X.ident[g] != 0);
-    const int nsm = tab_smem ? nsm_s[g] : __ldg(X.nsm + g);
-    const double* A = (tab_smem ? tab : X.mats) + (long long)g * 2 * O * O;
-    const double* B = A + O * O;
-    double* first = (NAPPLY == 2) ? bmid : bout;
-    x_row_apply<O>(cur, first, n_cells, nsm, ident, A, B, lane);
-    __syncwarp();
-    if (MOM) {
-      double s = 0.0;
-      for (int j = lane; j < row_len; j += 32) s = fma(first[j], xw_s[j], s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      const double wr = meta[1];
-      m0 += wr * s;
-      m1 = fma(wr * meta[2], s, m1);
-      m2 = fma(wr * meta[3], s, m2);
-    }
-    if (NAPPLY == 2) {
-      x_row_apply<O>(bmid, bout, n_cells, nsm, ident, A, B, lane);
-      __syncwarp();
-    }
-    double* dst = fout + r * ld_out;
-    if (VEC) {
-      for (int k = lane; k < row_len / 2; k += 32)
-        reinterpret_cast<double2*>(dst)[k] = reinterpret_cast<const double2*>(bout)[k];
-    } else {
-      for (int k = lane; k < row_len; k += 32) dst[k] = bout[k];
-    }
-    if (RHO) {
-      const double wr = meta[1];
-      for (int j = lane; j < row_len; j += 32) racc[j] = fma(wr, bout[j], racc[j]);
-    }
-    __syncwarp();
-  }
-  cp_wait<0>();
-  if (MOM && lane == 0) {
-    mom_red[warp][0] = m0;
-    mom_red[warp][1] = m1;
-    mom_red[warp][2] = m2;
-  }
-  __syncthreads();
-  if (MOM && threadIdx.x < 3) {
-    double s = 0.0;
-    for (int k = 0; k < nwarps; ++k) s += mom_red[k][threadIdx.x];
-    epi.mom_part[blockIdx.x * 3 + threadIdx.x] = s;
-  }
-  if (RHO) {
-    const long long roff = racc - wbase;
-    for (int j = threadIdx.x; j < row_len; j += blockDim.x) {
-      double s = 0.0;
-      for (int k = 0; k < nwarps; ++k)
-        s += sm[L.shared_dbl + (long long)k * L.per_warp_dbl + roff + j];
-      epi.rho_part[(long long)blockIdx.x * row_len + j] = s;
-    }
-  }
-}
+namespace sldg {
 
 // rho stage 1: CTA (chunk, 32-column tile), 8 warps stride the chunk's rows;
 // fixed-order smem combine -> partial[chunk][c]
@@ -606,21 +385,13 @@ template <int O, int NAPPLY, bool MOM, bool RHO>
 static int launch_xadv_t(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
                          long long ld_out, const XEpi& epi, const XadvGeom& g, bool vec,
                          cudaStream_t st) {
-  if (vec) {
-    auto k = k_xadv<O, NAPPLY, MOM, RHO, true>;
-    SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)std::max<size_t>(g.smem, 48 * 1024)));
-    k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
-                                          (int)X->n_cells, (int)X->n_speeds, g.tab_smem ? 1 : 0,
-                                          epi);
-  } else {
-    auto k = k_xadv<O, NAPPLY, MOM, RHO, false>;
-    SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)std::max<size_t>(g.smem, 48 * 1024)));
-    k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
-                                          (int)X->n_cells, (int)X->n_speeds, g.tab_smem ? 1 : 0,
-                                          epi);
-  }
+  const bool rreg = X->n_cells <= 32 * kRhoRegCells;
+  auto k = rreg ? k_xadv<O, NAPPLY, MOM, RHO, true> : k_xadv<O, NAPPLY, MOM, RHO, false>;
+  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(g.smem, 48 * 1024)));
+  k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
+                                        (int)X->n_cells, (int)X->n_speeds, g.tab_smem ? 1 : 0,
+                                        vec ? 1 : 0, epi);
   SLDG_LAUNCH_CHECK("k_xadv");
   return SLDG_OK;
 }
