@@ -346,7 +346,7 @@ static int launch_advect_x(const sldg_xplan* X, const double* fin, long long ld_
 }
 
 struct XadvGeom {
-  int wpb, grid;
+  int wpb, grid, cpcm;
   bool tab_smem;
   size_t smem;
   bool ok;
@@ -359,24 +359,26 @@ static XadvGeom xadv_geom(const sldg_xplan* X, int napply, bool rho) {
   (void)napply;
   (void)rho;
   XadvGeom g;
-  g.tab_smem = X->n_speeds * 2 * X->o * X->o * sizeof(double) <= 48 * 1024;
-  XadvLayout L = xadv_layout((int)X->n_cells, X->o, X->n_speeds, g.tab_smem);
+  g.tab_smem = X->n_speeds * 2 * X->o * X->o * sizeof(double) <= 32 * 1024;
+  XGeom G = x_geom((int)X->n_cells, X->o, X->n_speeds, g.tab_smem, 1 << 30);
+  g.cpcm = G.cpc <= 8 ? 8 : (G.cpc <= 16 ? 16 : 0);
   const size_t budget = 227 * 1024 - 1024;
   int best_w = 1, best_warps = 0;
   for (int w = 1; w <= 8; ++w) {
-    size_t smem = sizeof(double) * ((size_t)L.shared_dbl + (size_t)w * L.per_warp_dbl);
+    size_t smem = sizeof(double) * ((size_t)G.shared_dbl + (size_t)w * G.per_warp);
     if (smem > budget) break;
     int ctas = (int)std::min<size_t>(budget / smem, 8);
-    if (ctas * w > best_warps) {
+    if (ctas * w >= best_warps) {
       best_warps = ctas * w;
       best_w = w;
     }
   }
   g.wpb = best_w;
-  g.smem = sizeof(double) * ((size_t)L.shared_dbl + (size_t)g.wpb * L.per_warp_dbl);
-  g.ok = g.smem <= budget;
+  g.smem = sizeof(double) * ((size_t)G.shared_dbl + (size_t)g.wpb * G.per_warp);
+  g.ok = g.smem <= budget && g.cpcm > 0;
   const int ctas_per_sm = g.ok ? (int)std::max<size_t>(1, std::min<size_t>(8, budget / g.smem)) : 1;
-  long long want = (X->n_rows + g.wpb - 1) / g.wpb;
+  long long groups = (X->n_rows + G.rpw - 1) / G.rpw;
+  long long want = (groups + g.wpb - 1) / g.wpb;
   g.grid = (int)std::max<long long>(1, std::min<long long>(want, 148LL * ctas_per_sm));
   return g;
 }
@@ -385,13 +387,13 @@ template <int O, int NAPPLY, bool MOM, bool RHO>
 static int launch_xadv_t(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
                          long long ld_out, const XEpi& epi, const XadvGeom& g, bool vec,
                          cudaStream_t st) {
-  const bool rreg = X->n_cells <= 32 * kRhoRegCells;
-  auto k = rreg ? k_xadv<O, NAPPLY, MOM, RHO, true> : k_xadv<O, NAPPLY, MOM, RHO, false>;
+  (void)vec;
+  auto k = g.cpcm == 8 ? k_xadv<O, NAPPLY, MOM, RHO, 8> : k_xadv<O, NAPPLY, MOM, RHO, 16>;
   SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(g.smem, 48 * 1024)));
   k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
                                         (int)X->n_cells, (int)X->n_speeds, g.tab_smem ? 1 : 0,
-                                        vec ? 1 : 0, epi);
+                                        epi);
   SLDG_LAUNCH_CHECK("k_xadv");
   return SLDG_OK;
 }
@@ -569,7 +571,11 @@ int sldg_advect_x(const sldg_xplan* X, const double* fin, double* fout, int64_t 
   case O:                                                                           \
     if (xadv_geom(X, 1, false).ok) return launch_xadv<O>(X, fin, ld, fout, ld, 1, false, false, epi, st); \
     return launch_advect_x<O>(X, fin, ld, fout, ld, (int)X->n_cells, (int)X->n_cells, 0, 1, st);
-    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+    CASE(2) CASE(3) CASE(4)
+#undef CASE
+#define CASE(O) \
+  case O: return launch_advect_x<O>(X, fin, ld, fout, ld, (int)X->n_cells, (int)X->n_cells, 0, 1, st);
+    CASE(5) CASE(6)
 #undef CASE
   }
   set_error("unsupported degree");
@@ -606,11 +612,17 @@ int sldg_advect_x_fused(const sldg_xplan* X, const double* fin, double* fout, in
     epi.rho_part = (double*)scratch + 3 * (size_t)g.grid;
   }
   int rc = SLDG_ERR_UNSUPPORTED;
+  if (!g.ok) {
+    set_error("fused x pass: row too long for the shared-memory ring");
+    return rc;
+  }
   switch (X->o) {
 #define CASE(O) \
   case O: rc = launch_xadv<O>(X, fin, ld, fout, ld, n_apply, mom, rho, epi, st); break;
-    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+    CASE(2) CASE(3) CASE(4)
 #undef CASE
+    default:
+      set_error("fused x pass compiled for degree_x <= 3");
   }
   if (rc) return rc;
   if (mom) {
