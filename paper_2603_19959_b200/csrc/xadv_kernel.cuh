@@ -44,6 +44,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16x(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -74,7 +78,9 @@ __host__ __device__ inline XGeom x_geom(int n_cells, int o, long long n_speeds, 
   g.lpr = lpr;
   g.cpc = (n_cells + lpr - 1) / lpr;
   g.rpw = 32 / lpr;
-  g.cs = (g.cpc * o) | 1;
+  // chunk stride: 16-byte aligned when cpc*o is even (vector copies), with cs/2 odd so
+  // 8 lanes' 16-byte accesses fall in distinct bank groups; odd otherwise
+  g.cs = ((g.cpc * o) % 2 == 0) ? (((g.cpc * o) / 2) | 1) * 2 : g.cpc * o;
   g.rs = g.lpr * g.cs;
   g.slot = g.rpw * (g.rs + kXMeta);
   g.tab_dbl = tab_smem ? (int)(n_speeds * 2 * o * o) : 0;
@@ -129,6 +135,18 @@ k_xadv(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __re
   const long long gw = (long long)blockIdx.x * nwarps + warp;
   const long long tw = (long long)gridDim.x * nwarps;
 
+  // flat element -> padded offset: chunk = q / unit via a multiplicative inverse
+  const bool vec = (cpc_o % 2 == 0) && (ld_in % 2 == 0) && (ld_out % 2 == 0) &&
+                   ((((unsigned long long)fin) & 15) == 0) &&
+                   ((((unsigned long long)fout) & 15) == 0);
+  const unsigned unit = vec ? (unsigned)(cpc_o / 2) : (unsigned)cpc_o;   // copy units per chunk
+  const unsigned magic = 0xFFFFFFFFu / unit + 1u;
+  const int n_units = vec ? row_len / 2 : row_len;
+  auto pad_of = [&](int q) -> int {      // q: copy unit index within a row
+    const int ch = (int)__umulhi((unsigned)q, magic);
+    return ch * G.cs + (vec ? 2 : 1) * (q - ch * (int)unit);
+  };
+
   // stage RPW rows (group rg) + metadata into slot s
   auto issue = [&](long long rg, int s) {
     double* dst = wbase + s * G.slot;
@@ -137,8 +155,11 @@ k_xadv(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __re
       if (row >= n_rows) break;
       const double* src = fin + row * ld_in;
       double* drow = dst + r * G.rs;
-      for (int ch = 0; ch < G.lpr; ++ch)
-        for (int p = lane; p < cpc_o; p += 32) cp_async8(drow + ch * G.cs + p, src + ch * cpc_o + p);
+      if (vec) {
+        for (int q = lane; q < n_units; q += 32) cp_async16x(drow + pad_of(q), src + 2 * q);
+      } else {
+        for (int q = lane; q < n_units; q += 32) cp_async8(drow + pad_of(q), src + q);
+      }
       double* meta = dst + G.rpw * G.rs + r * kXMeta;
       if (lane == 0) cp_async4(meta, X.row_speed + row);
       if ((MOM || RHO) && lane == 1) cp_async8(meta + 1, epi.w + row);
@@ -269,8 +290,12 @@ k_xadv(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __re
       if (rr >= n_rows) break;
       const double* orow = out_base + r * G.rs;
       double* dst = fout + rr * ld_out;
-      for (int ch = 0; ch < G.lpr; ++ch)
-        for (int p = lane; p < cpc_o; p += 32) dst[ch * cpc_o + p] = orow[ch * G.cs + p];
+      if (vec) {
+        for (int q = lane; q < n_units; q += 32)
+          reinterpret_cast<double2*>(dst)[q] = *reinterpret_cast<const double2*>(orow + pad_of(q));
+      } else {
+        for (int q = lane; q < n_units; q += 32) dst[q] = orow[pad_of(q)];
+      }
     }
     (void)outrow;
     __syncwarp();
