@@ -85,7 +85,7 @@ __host__ __device__ inline XGeom x_geom(int n_cells, int o, long long n_speeds, 
   g.slot = g.rpw * (g.rs + kXMeta);
   g.tab_dbl = tab_smem ? (int)(n_speeds * 2 * o * o) : 0;
   const int small = tab_smem ? (int)((n_speeds * 5 + 7) / 8 + 1) : 0;
-  g.shared_dbl = g.tab_dbl + g.rs + small + 2;
+  g.shared_dbl = (g.tab_dbl + g.rs + small + 3) & ~1;   // keep per-warp slots 16-byte aligned
   g.per_warp = kXNBuf * g.slot + g.rpw * g.rs;
   return g;
 }
