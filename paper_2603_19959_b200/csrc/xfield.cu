@@ -355,13 +355,39 @@ struct XadvGeom {
 // Geometry depends only on the problem shape (never on the variant or the
 // device), so every variant shares one row->warp->CTA partition and the
 // fused reductions are bitwise reproducible.
-static XadvGeom xadv_geom(const sldg_xplan* X, int napply, bool rho) {
+// Rows of 8 x (power of two <= 32) cells with a shared-memory speed table use
+// the specialised k_xadv_c (compile-time chunk of 8 cells).
+static bool xadv_c_eligible(const sldg_xplan* X) {
+  const long long n = X->n_cells;
+  if (X->o < 2 || X->o > 4 || n % 8 != 0) return false;
+  const long long l = n / 8;
+  if (l < 1 || l > 32 || (l & (l - 1)) != 0) return false;
+  return X->n_speeds * 2 * X->o * X->o * sizeof(double) <= 32 * 1024;
+}
+
+static XadvGeom xadv_geom(const sldg_xplan* X, int napply, bool rho, bool allow_c = true) {
   (void)napply;
   (void)rho;
   XadvGeom g;
   g.tab_smem = X->n_speeds * 2 * X->o * X->o * sizeof(double) <= 32 * 1024;
   XGeom G = x_geom((int)X->n_cells, X->o, X->n_speeds, g.tab_smem, 1 << 30);
   g.cpcm = G.cpc <= 8 ? 8 : (G.cpc <= 16 ? 16 : 0);
+  int shared_dbl = G.shared_dbl, per_warp = G.per_warp, rpw = G.rpw;
+  if (allow_c && xadv_c_eligible(X)) {
+    g.cpcm = -8;   // marks the specialised kernel
+    XcGeom C;
+    switch (X->o) {
+      case 2: C = xc_geom<2, 8>((int)X->n_cells, X->n_speeds); break;
+      case 3: C = xc_geom<3, 8>((int)X->n_cells, X->n_speeds); break;
+      default: C = xc_geom<4, 8>((int)X->n_cells, X->n_speeds); break;
+    }
+    shared_dbl = C.shared_dbl;
+    per_warp = C.per_warp;
+    rpw = C.rpw;
+  }
+  G.shared_dbl = shared_dbl;
+  G.per_warp = per_warp;
+  G.rpw = rpw;
   const size_t budget = 227 * 1024 - 1024;
   int best_w = 1, best_warps = 0;
   for (int w = 1; w <= 8; ++w) {
@@ -375,7 +401,7 @@ static XadvGeom xadv_geom(const sldg_xplan* X, int napply, bool rho) {
   }
   g.wpb = best_w;
   g.smem = sizeof(double) * ((size_t)G.shared_dbl + (size_t)g.wpb * G.per_warp);
-  g.ok = g.smem <= budget && g.cpcm > 0;
+  g.ok = g.smem <= budget && g.cpcm != 0;
   const int ctas_per_sm = g.ok ? (int)std::max<size_t>(1, std::min<size_t>(8, budget / g.smem)) : 1;
   long long groups = (X->n_rows + G.rpw - 1) / G.rpw;
   long long want = (groups + g.wpb - 1) / g.wpb;
@@ -387,7 +413,15 @@ template <int O, int NAPPLY, bool MOM, bool RHO>
 static int launch_xadv_t(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
                          long long ld_out, const XEpi& epi, const XadvGeom& g, bool vec,
                          cudaStream_t st) {
-  (void)vec;
+  if (g.cpcm == -8) {
+    auto kc = k_xadv_c<O, NAPPLY, MOM, RHO, 8>;
+    SLDG_CUDA_TRY(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)std::max<size_t>(g.smem, 48 * 1024)));
+    kc<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
+                                           (int)X->n_cells, (int)X->n_speeds, epi);
+    SLDG_LAUNCH_CHECK("k_xadv_c");
+    return SLDG_OK;
+  }
   auto k = g.cpcm == 8 ? k_xadv<O, NAPPLY, MOM, RHO, 8> : k_xadv<O, NAPPLY, MOM, RHO, 16>;
   SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(g.smem, 48 * 1024)));
@@ -401,16 +435,12 @@ static int launch_xadv_t(const sldg_xplan* X, const double* fin, long long ld_in
 template <int O>
 static int launch_xadv(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
                        long long ld_out, int napply, bool mom, bool rho, const XEpi& epi,
-                       cudaStream_t st) {
-  XadvGeom g = xadv_geom(X, napply, rho);
+                       const XadvGeom& g, cudaStream_t st) {
   if (!g.ok) {
     set_error("x row too long for the pipelined x kernel");
     return SLDG_ERR_UNSUPPORTED;
   }
-  const int row_len = (int)(X->n_cells * O);
-  const bool vec = (row_len % 2 == 0) && (ld_in % 2 == 0) && (ld_out % 2 == 0) &&
-                   ((((unsigned long long)fin) & 15) == 0) &&
-                   ((((unsigned long long)fout) & 15) == 0);
+  const bool vec = true;
   int key = (napply == 2 ? 4 : 0) | (mom ? 2 : 0) | (rho ? 1 : 0);
   switch (key) {
     case 0: return launch_xadv_t<O, 1, false, false>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
@@ -423,6 +453,14 @@ static int launch_xadv(const sldg_xplan* X, const double* fin, long long ld_in, 
     case 7: return launch_xadv_t<O, 2, true, true>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
   }
   return SLDG_ERR_ARG;
+}
+
+// 16-byte-aligned rows: the specialised kernel is allowed (its geometry then fixes the
+// row partition of every pass on these buffers)
+static bool xadv_vec(const sldg_xplan* X, const double* fin, const double* fout, long long ld_in,
+                     long long ld_out) {
+  return ((X->n_cells * X->o) % 2 == 0) && (ld_in % 2 == 0) && (ld_out % 2 == 0) &&
+         ((((unsigned long long)fin) & 15) == 0) && ((((unsigned long long)fout) & 15) == 0);
 }
 
 }  // namespace sldg
@@ -569,7 +607,9 @@ int sldg_advect_x(const sldg_xplan* X, const double* fin, double* fout, int64_t 
   switch (X->o) {
 #define CASE(O)                                                                     \
   case O:                                                                           \
-    if (xadv_geom(X, 1, false).ok) return launch_xadv<O>(X, fin, ld, fout, ld, 1, false, false, epi, st); \
+    if (xadv_geom(X, 1, false).ok)                                                  \
+      return launch_xadv<O>(X, fin, ld, fout, ld, 1, false, false, epi,            \
+                            xadv_geom(X, 1, false, xadv_vec(X, fin, fout, ld, ld)), st); \
     return launch_advect_x<O>(X, fin, ld, fout, ld, (int)X->n_cells, (int)X->n_cells, 0, 1, st);
     CASE(2) CASE(3) CASE(4)
 #undef CASE
@@ -587,8 +627,8 @@ int sldg_xadv_scratch_bytes(const sldg_xplan* X, size_t* bytes) {
     set_error("bad argument");
     return SLDG_ERR_ARG;
   }
-  XadvGeom g = xadv_geom(X, 2, true);
-  *bytes = sizeof(double) * (size_t)g.grid * (3 + X->n_cells * X->o) + 256;
+  XadvGeom g = xadv_geom(X, 2, true, true), g2 = xadv_geom(X, 2, true, false);
+  *bytes = sizeof(double) * (size_t)std::max(g.grid, g2.grid) * (3 + X->n_cells * X->o) + 256;
   return SLDG_OK;
 }
 
@@ -605,7 +645,7 @@ int sldg_advect_x_fused(const sldg_xplan* X, const double* fin, double* fout, in
   }
   if (X->n_rows == 0) return SLDG_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  XadvGeom g = xadv_geom(X, n_apply, rho);
+  XadvGeom g = xadv_geom(X, n_apply, rho, xadv_vec(X, fin, fout, ld, ld));
   XEpi epi{w, v0, v2, xw, nullptr, nullptr};
   if (scratch) {
     epi.mom_part = (double*)scratch;
@@ -618,7 +658,7 @@ int sldg_advect_x_fused(const sldg_xplan* X, const double* fin, double* fout, in
   }
   switch (X->o) {
 #define CASE(O) \
-  case O: rc = launch_xadv<O>(X, fin, ld, fout, ld, n_apply, mom, rho, epi, st); break;
+  case O: rc = launch_xadv<O>(X, fin, ld, fout, ld, n_apply, mom, rho, epi, g, st); break;
     CASE(2) CASE(3) CASE(4)
 #undef CASE
     default:
