@@ -438,8 +438,8 @@ k_xadv_c(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __
                   fin + (row0 + r) * ld_in + 2 * us);
     }
     double* meta = dst + G.rpw * G.rs;
-    if (lane < 4 * nr) {
-      const int r = lane >> 2, fld = lane & 3;
+    for (int q = lane; q < 4 * nr; q += 32) {
+      const int r = q >> 2, fld = q & 3;
       const long long row = row0 + r;
       if (fld == 0) cp_async4(meta + r * kXMeta, X.row_speed + row);
       else if (fld == 1 && (MOM || RHO)) cp_async8(meta + r * kXMeta + 1, epi.w + row);
