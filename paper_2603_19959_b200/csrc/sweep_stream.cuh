@@ -1,0 +1,218 @@
+// sweep_stream.cuh -- streaming whole-pencil fast path of the v-sweep (included by vsweep.cu).
+//
+// Replaces the whole-pencil fast path of sweep_pencil (vsweep.py:197-200 ->
+// apply_update, sldg1d.py:124-136) for every pencil whose cells are all
+// conforming and on one level.  One CTA owns one pencil x one tile of up to
+// 256 x-columns; thread = column.  Each thread keeps its column's level
+// matrices A, B (2 o^2 fp64) in registers for the whole pencil.
+//
+// HBM streaming.  For direction 0 a cell's (p+1)^dim velocity rows are
+// consecutive rows of f, so a cell tile is (p+1)^dim rows x TX columns: when
+// the tile spans the full row (TX == ld) it is ONE contiguous block and is
+// fetched with ONE cp.async.bulk (the TMA engine, no per-thread address
+// generation); otherwise with one bulk copy per row.  Cells stream in pencil
+// order through a 4-slot ring tracked by mbarriers (transaction bytes), two
+// cells ahead of the compute, so every input coefficient is read from HBM
+// exactly once (absorbing bc; periodic re-reads the two wrap cells).  Outputs
+// go from registers to HBM with coalesced 8-byte stores (a warp writes 256
+// contiguous bytes per row).
+//
+// Valid when every active column of the tile has n_shift in {-1, 0} (all
+// Landau shifts; checked per tile): cell s then needs cells s-1, s, s+1.
+#pragma once
+
+namespace sldg {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA-engine bulk copy global -> shared, completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kStreamRing = 4;
+
+template <int O, int DIM>
+__global__ void __launch_bounds__(256, 1)
+k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
+               long long ld, long long n_cols, const double* __restrict__ speeds, int bc,
+               const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
+               double* __restrict__ acc, int tx_max, int n_tiles, int whole_rows) {
+  constexpr int NL = (DIM == 3) ? O * O : 1;
+  constexpr int NLOC = NL * O;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) unsigned long long full[kStreamRing];
+  __shared__ int s_nsmin, s_nsmax;
+
+  const long long wp = blockIdx.x / n_tiles;
+  const int tile = (int)(blockIdx.x - wp * n_tiles);
+  const long long q = P.walk_pencils[wp];
+  const long long off = P.p_off[q];
+  const int n = P.p_n[q];
+  const long long c0 = (long long)tile * tx_max;
+  const int tx = (int)min((long long)tx_max, n_cols - c0);
+  const int tid = threadIdx.x;
+  const int lev = P.e_level[off];
+  const int rstride = whole_rows ? (int)ld : tx_max;   // smem row stride (doubles)
+  const int cell_dbl = NLOC * rstride;
+  const unsigned cell_bytes = (unsigned)(NLOC * tx) * 8u;
+
+  if (tid == 0) {
+    s_nsmin = 1 << 30;
+    s_nsmax = -(1 << 30);
+    for (int k = 0; k < kStreamRing; ++k) mbar_init(&full[k], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const bool colv = tid < tx;
+  const long long c = c0 + tid;
+  const double speed = colv ? __ldg(speeds + c) : 0.0;
+  const long long ns = colv ? lm_ns[(long long)lev * n_cols + c] : 0;
+  if (colv && speed != 0.0) {
+    const int nsi = (int)max(min(ns, (long long)(1 << 29)), -(long long)(1 << 29));
+    atomicMin(&s_nsmin, nsi);
+    atomicMax(&s_nsmax, nsi);
+  }
+  __syncthreads();
+  const bool streamable = (s_nsmin >= -1 && s_nsmax <= 0) || (s_nsmin > s_nsmax);
+
+  double A[O * O], B[O * O];
+  if (colv) load_pair<O>(lm_mats, lev, n_cols, c, A, B);
+
+  if (!streamable) {
+    // arbitrary shifts in this tile: direct loads from HBM (same arithmetic)
+    if (!colv) return;
+    for (int s = 0; s < n; ++s) {
+      const long long e = off + s;
+      const int slot = P.e_slot[e];
+      double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c : acc + (long long)slot * NLOC * n_cols + c;
+      const long long dstride = slot < 0 ? ld : n_cols;
+      const double* self = fin + P.e_row0[e] * ld + c;
+      if (speed == 0.0) {
+        for (int r = 0; r < NLOC; ++r) dst[r * dstride] = self[r * ld];
+        continue;
+      }
+      long long qa = s - ns, qb = s - ns - 1;
+      bool va = true, vb = true;
+      if (bc == SLDG_BC_PERIODIC) { qa = pymod(qa, n); qb = pymod(qb, n); }
+      else { va = qa >= 0 && qa < n; vb = qb >= 0 && qb < n; }
+      const double* pa = fin + (va ? P.e_row0[off + qa] : 0) * ld + c;
+      const double* pb = fin + (vb ? P.e_row0[off + qb] : 0) * ld + c;
+      for (int t = 0; t < NL; ++t) {
+        double ua[O], ub[O], y[O];
+#pragma unroll
+        for (int i = 0; i < O; ++i) {
+          const int r = Lines<O, DIM>::row(P, t, i);
+          ua[i] = va ? pa[(long long)r * ld] : 0.0;
+          ub[i] = vb ? pb[(long long)r * ld] : 0.0;
+        }
+        two_cell<O>(A, B, ua, ub, va, vb, y);
+#pragma unroll
+        for (int i = 0; i < O; ++i) dst[(long long)Lines<O, DIM>::row(P, t, i) * dstride] = y[i];
+      }
+    }
+    return;
+  }
+
+  // load list: virtual cells v = -1 .. n (periodic) or 0 .. n-1 (absorbing); list
+  // position k holds virtual cell v0 + k in ring slot k % kStreamRing
+  const bool per = (bc == SLDG_BC_PERIODIC);
+  const int v0 = per ? -1 : 0;
+  const int n_load = per ? n + 2 : n;
+  auto issue = [&](int k) {   // called by warp 0 only
+    const int v = v0 + k;
+    const int cell = v < 0 ? n - 1 : (v >= n ? 0 : v);
+    double* dst = sm + (k % kStreamRing) * cell_dbl;
+    const double* src = fin + P.e_row0[off + cell] * ld + c0;
+    unsigned long long* bar = &full[k % kStreamRing];
+    if (whole_rows) {
+      if (tid == 0) {
+        mbar_expect_tx(bar, cell_bytes);
+        bulk_g2s(dst, src, cell_bytes, bar);
+      }
+    } else {
+      if (tid == 0) mbar_expect_tx(bar, cell_bytes);
+      __syncwarp();
+      for (int r = tid; r < NLOC; r += 32)
+        bulk_g2s(dst + r * rstride, src + (long long)r * ld, (unsigned)tx * 8u, bar);
+    }
+  };
+  if (tid < 32) {
+    for (int k = 0; k < min(3, n_load); ++k) issue(k);
+  }
+  // per-line row offsets (compile-time for direction 0)
+  for (int s = 0; s < n; ++s) {
+    // prefetch list position of virtual cell s+2
+    const int kn = s + 2 - v0;
+    if (tid < 32 && kn < n_load && kn >= 3) issue(kn);
+    // wait for virtual cells s-1 .. s+1 that exist in the list
+    const int klo = max(s - 1 - v0, 0), khi = min(s + 1 - v0, n_load - 1);
+    for (int k = klo; k <= khi; ++k) mbar_wait(&full[k % kStreamRing], (unsigned)((k / kStreamRing) & 1));
+    if (colv) {
+      const long long e = off + s;
+      const int slot = P.e_slot[e];
+      double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c
+                             : acc + (long long)slot * NLOC * n_cols + c;
+      const long long dstride = slot < 0 ? ld : n_cols;
+      const double* me = sm + ((s - v0) % kStreamRing) * cell_dbl + tid;
+      if (speed == 0.0) {
+#pragma unroll 3
+        for (int r = 0; r < NLOC; ++r) dst[r * dstride] = me[r * rstride];
+      } else {
+        // sources: virtual cells s - ns (same) and s - ns - 1 (neighbour)
+        const int va_cell = s - (int)ns, vb_cell = s - (int)ns - 1;
+        const bool va = per || (va_cell >= 0 && va_cell < n);
+        const bool vb = per || (vb_cell >= 0 && vb_cell < n);
+        const double* sa = sm + ((va ? va_cell : s) - v0) % kStreamRing * cell_dbl + tid;
+        const double* sb = sm + ((vb ? vb_cell : s) - v0) % kStreamRing * cell_dbl + tid;
+#pragma unroll
+        for (int t = 0; t < NL; ++t) {
+          double ua[O], ub[O], y[O];
+#pragma unroll
+          for (int i = 0; i < O; ++i) {
+            const int r = (DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i;
+            ua[i] = va ? sa[r * rstride] : 0.0;
+            ub[i] = vb ? sb[r * rstride] : 0.0;
+          }
+          two_cell<O>(A, B, ua, ub, va, vb, y);
+#pragma unroll
+          for (int i = 0; i < O; ++i) {
+            const int r = (DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i;
+            dst[(long long)r * dstride] = y[i];
+          }
+        }
+      }
+    }
+    __syncthreads();   // slot of virtual cell s-1 is refilled next iteration
+  }
+}
+
+}  // namespace sldg

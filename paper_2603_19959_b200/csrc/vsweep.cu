@@ -339,186 +339,11 @@ k_sweep_generic(VPlanDev P, DevBasis b, const double* __restrict__ fin,
                       lm_ns, lm_mats, acc);
 }
 
-// ---------------------------------------------------------------------------
-// Whole-pencil fast path: one CTA = one pencil x one tile of TX columns, all
-// lines.  Cells are streamed in pencil order into a shared-memory ring with
-// cp.async (16 B, L1-bypassing); each cell of the pencil is read from HBM
-// exactly once, the wrap cells of a periodic pencil are kept resident.  Each
-// thread owns one column (matrices in registers) and a subset of lines.
-// Valid when every column of the tile has n_shift in [-1, 0] (the Landau
-// regime; checked per tile, the kernel falls back to direct loads otherwise).
-// ---------------------------------------------------------------------------
-template <int O, int DIM, int TX>
-struct WalkCfg {
-  static constexpr int NL = Lines<O, DIM>::NL;
-  static constexpr int NLOC = NL * O;
-  static constexpr int RING = 4;                 // cells resident (s-1, s, s+1, prefetch)
-  static constexpr int CELL_DBL = NLOC * TX;     // doubles per staged cell tile
-};
+}  // namespace sldg
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
+#include "sweep_stream.cuh"
 
-template <int O, int DIM, int TX>
-__global__ void __launch_bounds__(256)
-k_sweep_walk(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
-             long long ld, long long n_cols, const double* __restrict__ speeds, int bc,
-             const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
-             double* __restrict__ acc, int n_tiles) {
-  using C = WalkCfg<O, DIM, TX>;
-  extern __shared__ __align__(16) double smem[];
-  // ring slots 0..RING-1, then 2 wrap slots (first cell, last cell of the pencil)
-  double* ring = smem;
-  double* wrap0 = smem + C::RING * C::CELL_DBL;
-  double* wrapN = wrap0 + C::CELL_DBL;
-  __shared__ int s_nsmin, s_nsmax;
-
-  const long long wp = blockIdx.x / n_tiles;
-  const int tile = blockIdx.x - (int)(wp * n_tiles);
-  const long long q = P.walk_pencils[wp];
-  const long long off = P.p_off[q];
-  const int n = P.p_n[q];
-  const long long c0 = (long long)tile * TX;
-  const int tx = (int)min((long long)TX, n_cols - c0);   // columns in this tile
-  const int tid = threadIdx.x;
-  const int lev = P.e_level[off];
-
-  if (tid == 0) { s_nsmin = 1 << 30; s_nsmax = -(1 << 30); }
-  __syncthreads();
-  // thread -> (column, line phase)
-  const int col = tid % TX;
-  const int phase = tid / TX;
-  constexpr int PHASES = 256 / TX;
-  const bool colv = col < tx;
-  const long long c = c0 + col;
-  double speed = colv ? __ldg(speeds + c) : 0.0;
-  long long ns = colv ? lm_ns[(long long)lev * n_cols + c] : 0;
-  if (colv && speed != 0.0) {
-    atomicMin(&s_nsmin, (int)max(min(ns, (long long)(1 << 29)), -(long long)(1 << 29)));
-    atomicMax(&s_nsmax, (int)max(min(ns, (long long)(1 << 29)), -(long long)(1 << 29)));
-  }
-  __syncthreads();
-  const bool window_ok = (s_nsmin >= -1 && s_nsmax <= 0) || (s_nsmin > s_nsmax);
-  const bool vec_ok = ((ld & 1) == 0) && ((tx & 1) == 0) && ((c0 & 1) == 0) &&
-                      ((((unsigned long long)fin) & 15) == 0);
-
-  double A[O * O], B[O * O];
-  if (colv) load_pair<O>(lm_mats, lev, n_cols, c, A, B);
-
-  if (!window_ok || !vec_ok) {
-    // direct-load fallback for this tile (arbitrary shifts)
-    if (!colv) return;
-    for (int s = 0; s < n; ++s) {
-      const long long e = off + s;
-      const int slot = P.e_slot[e];
-      double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c
-                             : acc + (long long)slot * C::NLOC * n_cols + c;
-      const long long dstride = slot < 0 ? ld : n_cols;
-      const double* self = fin + P.e_row0[e] * ld + c;
-      if (speed == 0.0) {
-        for (int r = phase; r < C::NLOC; r += PHASES) dst[r * dstride] = self[r * ld];
-        continue;
-      }
-      long long qa = s - ns, qb = s - ns - 1;
-      bool va = true, vb = true;
-      if (bc == SLDG_BC_PERIODIC) { qa = pymod(qa, n); qb = pymod(qb, n); }
-      else { va = qa >= 0 && qa < n; vb = qb >= 0 && qb < n; }
-      const double* pa = fin + (va ? P.e_row0[off + qa] : 0) * ld + c;
-      const double* pb = fin + (vb ? P.e_row0[off + qb] : 0) * ld + c;
-      for (int t = phase; t < C::NL; t += PHASES) {
-        double ua[O], ub[O], y[O];
-#pragma unroll
-        for (int i = 0; i < O; ++i) {
-          int r = Lines<O, DIM>::row(P, t, i);
-          ua[i] = va ? pa[(long long)r * ld] : 0.0;
-          ub[i] = vb ? pb[(long long)r * ld] : 0.0;
-        }
-        two_cell<O>(A, B, ua, ub, va, vb, y);
-#pragma unroll
-        for (int i = 0; i < O; ++i) dst[(long long)Lines<O, DIM>::row(P, t, i) * dstride] = y[i];
-      }
-    }
-    return;
-  }
-
-  // ---- staged walk: cell j of the pencil lives in ring slot j % RING ----
-  // tile of one cell in smem: [local row r][col] (TX doubles per row)
-  auto stage = [&](int j, double* buf) {
-    const double* g = fin + P.e_row0[off + j] * ld + c0;
-    constexpr int V = TX / 2;                      // 16-byte chunks per row
-    const int chunks = C::NLOC * (tx / 2);
-    for (int k = tid; k < chunks; k += 256) {
-      int r = k / (tx / 2), v = k - r * (tx / 2);
-      cp_async16(buf + r * TX + 2 * v, g + (long long)r * ld + 2 * v);
-    }
-    (void)V;
-  };
-  auto slot_of = [&](int j) -> double* {
-    if (bc == SLDG_BC_PERIODIC) {
-      if (j == 0) return wrap0;
-      if (j == n - 1) return wrapN;
-    }
-    return ring + (j % C::RING) * C::CELL_DBL;
-  };
-  // prologue: wrap cells (periodic), then cells 0, 1 (ring)
-  if (bc == SLDG_BC_PERIODIC) {
-    stage(0, wrap0);
-    if (n > 1) stage(n - 1, wrapN);
-  }
-  cp_async_commit();
-  for (int j = 0; j < 2; ++j) {
-    if (j < n && !(bc == SLDG_BC_PERIODIC && (j == 0 || j == n - 1))) stage(j, slot_of(j));
-    cp_async_commit();
-  }
-  for (int s = 0; s < n; ++s) {
-    // prefetch cell s+2 (needed by s+1 when ns = -1 reads s+2)
-    const int jn = s + 2;
-    if (jn < n && !(bc == SLDG_BC_PERIODIC && (jn == 0 || jn == n - 1))) stage(jn, slot_of(jn));
-    cp_async_commit();
-    cp_async_wait<1>();       // everything up to cell s+1 landed
-    __syncthreads();
-    const long long e = off + s;
-    const int slot = P.e_slot[e];
-    if (colv) {
-      double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c
-                             : acc + (long long)slot * C::NLOC * n_cols + c;
-      const long long dstride = slot < 0 ? ld : n_cols;
-      if (speed == 0.0) {
-        const double* me = slot_of(s) + col;
-        for (int r = phase; r < C::NLOC; r += PHASES) dst[r * dstride] = me[r * TX];
-      } else {
-        long long qa = s - ns, qb = s - ns - 1;
-        bool va = true, vb = true;
-        if (bc == SLDG_BC_PERIODIC) { qa = pymod(qa, n); qb = pymod(qb, n); }
-        else { va = qa >= 0 && qa < n; vb = qb >= 0 && qb < n; }
-        const double* sa = slot_of(va ? (int)qa : s) + col;
-        const double* sb = slot_of(vb ? (int)qb : s) + col;
-        for (int t = phase; t < C::NL; t += PHASES) {
-          double ua[O], ub[O], y[O];
-#pragma unroll
-          for (int i = 0; i < O; ++i) {
-            int r = Lines<O, DIM>::row(P, t, i);
-            ua[i] = va ? sa[r * TX] : 0.0;
-            ub[i] = vb ? sb[r * TX] : 0.0;
-          }
-          two_cell<O>(A, B, ua, ub, va, vb, y);
-#pragma unroll
-          for (int i = 0; i < O; ++i)
-            dst[(long long)Lines<O, DIM>::row(P, t, i) * dstride] = y[i];
-        }
-      }
-    }
-    __syncthreads();          // ring slot of cell s-1 may be overwritten next
-  }
-  cp_async_wait<0>();
-}
+namespace sldg {
 
 // weighted write-back (vsweep.py:403-409): out = ((f_in + S_g1) + S_g2) + ...,
 // S_g = sum over the group's contributions in flat order of w (r - f_in).
@@ -599,18 +424,35 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
                         const long long* lm_ns, const double* lm_mats, double* acc,
                         cudaStream_t st) {
   constexpr int NLOC = Lines<O, DIM>::NLOC;
-  constexpr int TX = 32;
-  using C = WalkCfg<O, DIM, TX>;
-  const size_t smem = sizeof(double) * (size_t)(C::RING + 2) * C::CELL_DBL;
-  const bool use_walk = !force_slow && p->n_walk > 0 && n_cols >= 2 && smem <= 200 * 1024;
-  if (use_walk) {
-    SLDG_CUDA_TRY(cudaFuncSetAttribute(k_sweep_walk<O, DIM, TX>,
+  // streaming kernel geometry: whole rows per cell when the tile spans the row
+  // (one bulk copy per cell), else column tiles with one bulk copy per row
+  const size_t budget = 227 * 1024 - 256;
+  const bool al16 = ((((unsigned long long)fin) & 15) == 0) && (ld % 2 == 0);
+  int tx_max = 0, whole = 0;
+  if (al16 && n_cols == ld && n_cols <= 256 && (NLOC * n_cols) % 2 == 0 &&
+      sizeof(double) * kStreamRing * NLOC * n_cols <= budget) {
+    tx_max = (int)n_cols;
+    whole = 1;
+  } else if (al16 && n_cols % 2 == 0) {
+    for (int t = 256; t >= 32; t -= 32)
+      if (sizeof(double) * kStreamRing * NLOC * t <= budget) {
+        tx_max = t;
+        break;
+      }
+    if (tx_max > n_cols) tx_max = (int)((n_cols + 31) / 32 * 32);
+  }
+  const bool use_stream = !force_slow && p->n_walk > 0 && tx_max > 0 && n_cols >= 2;
+  if (use_stream) {
+    const int threads = (tx_max + 31) / 32 * 32;
+    const int rstride = whole ? (int)ld : tx_max;
+    const size_t smem = sizeof(double) * (size_t)kStreamRing * NLOC * rstride;
+    SLDG_CUDA_TRY(cudaFuncSetAttribute(k_sweep_stream<O, DIM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int n_tiles = (int)((n_cols + TX - 1) / TX);
-    long long blocks = p->n_walk * n_tiles;
-    k_sweep_walk<O, DIM, TX><<<(unsigned)blocks, 256, smem, st>>>(
-        p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, n_tiles);
-    SLDG_LAUNCH_CHECK("k_sweep_walk");
+    const int n_tiles = (int)((n_cols + tx_max - 1) / tx_max);
+    const long long blocks = p->n_walk * n_tiles;
+    k_sweep_stream<O, DIM><<<(unsigned)blocks, threads, smem, st>>>(
+        p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, tx_max, n_tiles, whole);
+    SLDG_LAUNCH_CHECK("k_sweep_stream");
     if (p->n_gen > 0) {
       long long n = p->n_gen * n_cols;
       k_sweep_generic<O, DIM><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
