@@ -25,6 +25,8 @@
 
 #include <algorithm>
 
+#include "tma_util.cuh"
+
 namespace sldg {
 
 struct XEpi {
@@ -356,14 +358,18 @@ k_xadv(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __re
 namespace sldg {
 
 // ---------------------------------------------------------------------------
-// Specialised variant for rows whose cell count is CPC x (power of two <= 32):
-// CPC is a compile-time constant, every row carries a ghost copy of its first
-// chunk after the last one (so a lane's CPC+1 source cells never wrap), the
-// matrices load as 16-byte vectors, outputs go from registers straight to HBM.
+// Specialised variant for rows of CPC x (power of two <= 32) cells, CPC = 8.
+// Every row chunk (CPC*O doubles, 16-byte aligned in HBM) is fetched by one
+// lane with a cp.async.bulk (TMA engine) into the padded shared-memory slot,
+// plus a ghost copy of chunk 0 after the last chunk, so a lane's CPC+1
+// source cells never wrap.  Completion: one mbarrier per slot (transaction
+// bytes).  Row metadata (speed index, weights) is prefetched into registers
+// one iteration ahead.  For X.X the intermediate row is written back into the
+// consumed slot.  Outputs go from registers straight to HBM (16-byte stores).
 // Same arithmetic as k_xadv (bitwise-identical results and reductions).
 // ---------------------------------------------------------------------------
 struct XcGeom {
-  int lpr, rpw, cs, rs, unit, n_units, g_units, slot, shared_dbl, per_warp, tab_dbl;
+  int lpr, rpw, cs, rs, slot, shared_dbl, per_warp, tab_dbl;
 };
 
 template <int O, int CPC>
@@ -374,14 +380,11 @@ __host__ __device__ inline XcGeom xc_geom(int n_cells, long long n_speeds) {
   constexpr int CO = CPC * O;
   g.cs = (CO % 2 == 0) ? ((CO / 2) | 1) * 2 : CO;     // see x_geom
   g.rs = (g.lpr + 1) * g.cs;                         // + ghost chunk
-  g.unit = CO / 2;                                   // 16-byte units per chunk (CO even)
-  g.n_units = n_cells * O / 2;
-  g.g_units = g.n_units + g.unit;                    // with the ghost
-  g.slot = g.rpw * g.rs + ((g.rpw * kXMeta + 1) & ~1);
+  g.slot = g.rpw * g.rs;
   g.tab_dbl = (int)(n_speeds * 2 * O * O);
   const int small = (int)((n_speeds * 5 + 7) / 8 + 1);
-  g.shared_dbl = (g.tab_dbl + small + 1) & ~1;
-  g.per_warp = kXNBuf * g.slot + g.rpw * g.rs;
+  g.shared_dbl = (g.tab_dbl + n_cells * O + small + 1) & ~1;   // table, x weights, shifts
+  g.per_warp = kXNBuf * g.slot;
   return g;
 }
 
@@ -391,15 +394,17 @@ k_xadv_c(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __
          long long ld_out, long long n_rows, int n_cells, int n_speeds, XEpi epi) {
   constexpr int CO = CPC * O;
   static_assert(CO % 2 == 0, "vector path needs an even chunk length");
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) double sm[];
   const XcGeom G = xc_geom<O, CPC>(n_cells, n_speeds);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int grp = lane / G.lpr, sub = lane - grp * G.lpr;
+  const int row_len = n_cells * O;
   double* tab = sm;
-  int* nsm_s = reinterpret_cast<int*>(sm + G.tab_dbl);
+  double* xw_s = sm + G.tab_dbl;
+  int* nsm_s = reinterpret_cast<int*>(xw_s + row_len);
   unsigned char* id_s = reinterpret_cast<unsigned char*>(nsm_s + n_speeds);
   double* wbase = sm + G.shared_dbl + (long long)warp * G.per_warp;
-  double* bmid = wbase + kXNBuf * G.slot;
+  __shared__ __align__(8) unsigned long long full[8][kXNBuf];
   __shared__ double mom_red[8][3];
 
   for (int q = threadIdx.x; q < G.tab_dbl; q += blockDim.x) tab[q] = __ldg(X.mats + q);
@@ -407,10 +412,11 @@ k_xadv_c(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __
     nsm_s[q] = __ldg(X.nsm + q);
     id_s[q] = X.ident[q];
   }
-  double xwr[MOM ? CO : 1];
-  if (MOM) {
-#pragma unroll
-    for (int q = 0; q < CO; ++q) xwr[q] = __ldg(epi.xw + sub * CO + q);
+  if (MOM)
+    for (int q = threadIdx.x; q < row_len; q += blockDim.x) xw_s[q] = __ldg(epi.xw + q);
+  if (lane == 0) {
+    for (int k = 0; k < kXNBuf; ++k) mbar_init(&full[warp][k], 1);
+    mbar_fence_init();
   }
   double racc[RHO ? CO : 1];
 #pragma unroll
@@ -420,35 +426,43 @@ k_xadv_c(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __
   const long long ngroups = (n_rows + G.rpw - 1) / G.rpw;
   const long long gw = (long long)blockIdx.x * nwarps + warp;
   const long long tw = (long long)gridDim.x * nwarps;
-  const unsigned magic_u = 0xFFFFFFFFu / (unsigned)G.unit + 1u;
-  const unsigned magic_r = 0xFFFFFFFFu / (unsigned)G.g_units + 1u;
   double m0 = 0.0, m1 = 0.0, m2 = 0.0;
+  const int chunks = G.lpr + 1;
 
+  // bulk-copy row group rg into slot s: lane q -> (row q / chunks, chunk q % chunks)
   auto issue = [&](long long rg, int s) {
     double* dst = wbase + s * G.slot;
     const long long row0 = rg * G.rpw;
     const int nr = (int)min((long long)G.rpw, n_rows - row0);
-    const int total = nr * G.g_units;
-    for (int q = lane; q < total; q += 32) {
-      const int r = (int)__umulhi((unsigned)q, magic_r);
-      const int u = q - r * G.g_units;                         // unit within row (+ghost)
-      const int ch = (int)__umulhi((unsigned)u, magic_u);
-      const int us = u < G.n_units ? u : u - G.n_units;        // ghost re-reads chunk 0
-      cp_async16x(dst + r * G.rs + ch * G.cs + 2 * (u - ch * G.unit),
-                  fin + (row0 + r) * ld_in + 2 * us);
-    }
-    double* meta = dst + G.rpw * G.rs;
-    for (int q = lane; q < 4 * nr; q += 32) {
-      const int r = q >> 2, fld = q & 3;
-      const long long row = row0 + r;
-      if (fld == 0) cp_async4(meta + r * kXMeta, X.row_speed + row);
-      else if (fld == 1 && (MOM || RHO)) cp_async8(meta + r * kXMeta + 1, epi.w + row);
-      else if (fld == 2 && MOM) cp_async8(meta + r * kXMeta + 2, epi.v0 + row);
-      else if (fld == 3 && MOM) cp_async8(meta + r * kXMeta + 3, epi.v2 + row);
+    if (lane == 0) mbar_expect_tx(&full[warp][s], (unsigned)(nr * chunks * CO * 8));
+    __syncwarp();
+    for (int q = lane; q < nr * chunks; q += 32) {
+      const int r = q / chunks, ch = q - r * chunks;
+      const int chs = ch < G.lpr ? ch : 0;          // ghost re-reads chunk 0
+      bulk_g2s(dst + r * G.rs + ch * G.cs, fin + (row0 + r) * ld_in + chs * CO,
+               (unsigned)(CO * 8), &full[warp][s]);
     }
   };
+  // per-row metadata for this lane's row of group rg
+  struct Meta {
+    int g;
+    double w, v0, v2;
+  };
+  auto fetch_meta = [&](long long rg) {
+    Meta m{0, 0.0, 0.0, 0.0};
+    const long long row = rg * G.rpw + grp;
+    if (rg < ngroups && row < n_rows) {
+      m.g = __ldg(X.row_speed + row);
+      if (MOM || RHO) m.w = __ldg(epi.w + row);
+      if (MOM) {
+        m.v0 = __ldg(epi.v0 + row);
+        m.v2 = __ldg(epi.v2 + row);
+      }
+    }
+    return m;
+  };
 
-  // one application on this lane's chunk; src row has the ghost chunk
+  // one application on this lane's chunk (src row with ghost); y: CO outputs
   auto apply = [&](const double* srow, int nsm, bool ident, const double* AB, double* y) {
     if (ident) {
 #pragma unroll
@@ -492,56 +506,47 @@ k_xadv_c(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __
     }
   };
 
-#pragma unroll
   for (int p = 0; p < kXNBuf - 1; ++p) {
     long long rg = gw + p * tw;
     if (rg < ngroups) issue(rg, p);
-    cp_commit();
   }
+  Meta meta = fetch_meta(gw);
   int it = 0;
   for (long long rg = gw; rg < ngroups; rg += tw, ++it) {
-    long long rn = rg + (kXNBuf - 1) * tw;
+    const long long rn = rg + (kXNBuf - 1) * tw;
     if (rn < ngroups) issue(rn, (it + kXNBuf - 1) % kXNBuf);
-    cp_commit();
-    cp_wait<kXNBuf - 1>();
-    __syncwarp();
-    const double* cur = wbase + (it % kXNBuf) * G.slot;
+    const Meta next = fetch_meta(rg + tw);
+    const int s = it % kXNBuf;
+    mbar_wait(&full[warp][s], (unsigned)((it / kXNBuf) & 1));
+    double* cur = wbase + s * G.slot;
     const long long row = rg * G.rpw + grp;
     const bool live = row < n_rows;
-    double s_mom = 0.0, wr = 0.0, v0r = 0.0, v2r = 0.0;
+    double s_mom = 0.0;
     double y[CO];
-    int nsm = 0;
-    bool ident = true;
-    const double* AB = tab;
+    const int g = meta.g;
+    const bool ident = id_s[g] != 0;
+    const int nsm = nsm_s[g];
+    const double* AB = tab + (long long)g * 2 * O * O;
+    double* srow = cur + grp * G.rs;
     if (live) {
-      const double* meta = cur + G.rpw * G.rs + grp * kXMeta;
-      const int g = *reinterpret_cast<const int*>(meta);
-      if (MOM || RHO) wr = meta[1];
-      if (MOM) {
-        v0r = meta[2];
-        v2r = meta[3];
-      }
-      ident = id_s[g] != 0;
-      nsm = nsm_s[g];
-      AB = tab + (long long)g * 2 * O * O;
-      apply(cur + grp * G.rs, nsm, ident, AB, y);
+      apply(srow, nsm, ident, AB, y);
       if (MOM) {
 #pragma unroll
-        for (int q = 0; q < CO; ++q) s_mom = fma(y[q], xwr[q], s_mom);
+        for (int q = 0; q < CO; ++q) s_mom = fma(y[q], xw_s[sub * CO + q], s_mom);
       }
     }
     if (NAPPLY == 2) {
-      double* mrow = bmid + grp * G.rs;
+      __syncwarp();                     // every lane has read its sources
       if (live) {
 #pragma unroll
-        for (int q = 0; q < CO; ++q) mrow[sub * G.cs + q] = y[q];
+        for (int q = 0; q < CO; ++q) srow[sub * G.cs + q] = y[q];
         if (sub == 0) {
 #pragma unroll
-          for (int q = 0; q < CO; ++q) mrow[G.lpr * G.cs + q] = y[q];   // ghost
+          for (int q = 0; q < CO; ++q) srow[G.lpr * G.cs + q] = y[q];   // ghost
         }
       }
       __syncwarp();
-      if (live) apply(mrow, nsm, ident, AB, y);
+      if (live) apply(srow, nsm, ident, AB, y);
     }
     if (live) {
       double* dst = fout + row * ld_out + sub * CO;
@@ -550,20 +555,20 @@ k_xadv_c(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __
         reinterpret_cast<double2*>(dst)[q] = make_double2(y[2 * q], y[2 * q + 1]);
       if (RHO) {
 #pragma unroll
-        for (int q = 0; q < CO; ++q) racc[q] = fma(wr, y[q], racc[q]);
+        for (int q = 0; q < CO; ++q) racc[q] = fma(meta.w, y[q], racc[q]);
       }
     }
     if (MOM) {
       for (int o = G.lpr >> 1; o > 0; o >>= 1) s_mom += __shfl_xor_sync(0xffffffffu, s_mom, o);
       if (live) {
-        m0 += wr * s_mom;
-        m1 = fma(wr * v0r, s_mom, m1);
-        m2 = fma(wr * v2r, s_mom, m2);
+        m0 += meta.w * s_mom;
+        m1 = fma(meta.w * meta.v0, s_mom, m1);
+        m2 = fma(meta.w * meta.v2, s_mom, m2);
       }
     }
-    __syncwarp();
+    meta = next;
+    __syncwarp();                       // slot s is refilled next iteration
   }
-  cp_wait<0>();
   if (MOM) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
     for (int q = 0; q < G.rpw; ++q) {
@@ -577,13 +582,14 @@ k_xadv_c(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __
       mom_red[warp][2] = a2;
     }
   }
-  if (RHO) {   // per-warp column partial = sum over row groups in order -> bmid (dense)
+  if (RHO) {   // per-warp column partial = sum over row groups in order -> slot 0 (dense)
+    double* part = wbase;
     for (int q = 0; q < G.rpw; ++q) {
       if (grp == q) {
 #pragma unroll
         for (int k = 0; k < CO; ++k) {
           const int off = sub * CO + k;
-          bmid[off] = (q == 0) ? racc[k] : bmid[off] + racc[k];
+          part[off] = (q == 0) ? racc[k] : part[off] + racc[k];
         }
       }
       __syncwarp();
@@ -596,11 +602,9 @@ k_xadv_c(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __
     epi.mom_part[blockIdx.x * 3 + threadIdx.x] = s;
   }
   if (RHO) {
-    const int row_len = n_cells * O;
     for (int e = threadIdx.x; e < row_len; e += blockDim.x) {
       double s = 0.0;
-      for (int q = 0; q < nwarps; ++q)
-        s += sm[G.shared_dbl + (long long)q * G.per_warp + kXNBuf * G.slot + e];
+      for (int q = 0; q < nwarps; ++q) s += sm[G.shared_dbl + (long long)q * G.per_warp + e];
       epi.rho_part[(long long)blockIdx.x * row_len + e] = s;
     }
   }
