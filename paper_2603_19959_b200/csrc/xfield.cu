@@ -311,10 +311,11 @@ __global__ void k_field_diag(const double* __restrict__ e, const double* __restr
 
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+// The row partition depends on n_rows only, so every column's rho is bitwise
+// identical however the columns are sharded across ranks.
 static long long rho_chunks(long long n_rows, long long n_cols) {
-  long long tiles = (n_cols + 31) / 32;
-  long long want = std::max<long long>(1, (148LL * 8 + tiles - 1) / tiles);
-  long long chunk = std::max<long long>(64, (n_rows + want - 1) / want);
+  (void)n_cols;
+  long long chunk = std::max<long long>(64, (n_rows + 255) / 256);
   return (n_rows + chunk - 1) / chunk;
 }
 
