@@ -145,7 +145,10 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfgd = CONFIGS[args.config]
+    cfgd = dict(CONFIGS[args.config])
+    if world > 1:
+        # weak scaling: every rank keeps the N=1 slab (N_x grows with the rank count)
+        cfgd["n_x"] = cfgd["n_x"] * world
     cfg = sv.SimConfig(**cfgd, n_steps=args.steps)
     if world > 1:
         from paper_2603_19959_b200.shard import ShardedSimulation

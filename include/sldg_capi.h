@@ -180,6 +180,10 @@ int sldg_poisson_efield(const sldg_poisson* p, const double* phi, double* e, voi
 int sldg_field_diag(const sldg_poisson* p, const double* e, double* out2, void* stream);
 
 /* ---------------------------------------------------------------- misc */
+/* out[i*ld + j] = a[i] * b[j]: the separable initial condition sampled on the
+ * device (sample_initial, driver.py:132-136), bit-identical to numpy's product. */
+int sldg_outer(const double* a, int64_t na, const double* b, int64_t nb, double* out, int64_t ld,
+               void* stream);
 const char* sldg_last_error(void);
 int sldg_version(void);
 /* number of kernel launches enqueued by this library since load (for bench) */

@@ -69,6 +69,8 @@ _SIGS = {
     "sldg_version": (C.c_int, []),
     "sldg_last_error": (C.c_char_p, []),
     "sldg_launch_count": (C.c_int64, []),
+    "sldg_outer": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                             C.c_int64, C.c_void_p]),
     "sldg_overlap_pairs": (C.c_int, [C.POINTER(SldgBasis), C.c_void_p, C.c_int64, C.c_void_p,
                                      C.c_void_p, C.c_void_p]),
     "sldg_vplan_create": (C.c_int, [C.POINTER(SldgVPlanDesc), C.POINTER(C.c_void_p)]),

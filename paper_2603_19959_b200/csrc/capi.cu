@@ -60,6 +60,15 @@ __global__ void k_overlap_pairs(DevBasis b, const double* __restrict__ fracs, lo
   }
 }
 
+// out[i, j] = a[i] * b[j]  (sample_initial, driver.py:132-136: gv[:, None] * gx[None, :])
+__global__ void k_outer(const double* __restrict__ a, long long na, const double* __restrict__ b,
+                        long long nb, double* __restrict__ out, long long ld) {
+  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= na * nb) return;
+  long long i = idx / nb, j = idx - i * nb;
+  out[i * ld + j] = a[i] * b[j];
+}
+
 }  // namespace sldg
 
 using namespace sldg;
@@ -71,6 +80,19 @@ const char* sldg_last_error(void) { return g_last_error.c_str(); }
 int sldg_version(void) { return 10000; }
 
 int64_t sldg_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int sldg_outer(const double* a, int64_t na, const double* b, int64_t nb, double* out, int64_t ld,
+               void* stream) {
+  if (!a || !b || !out || na < 0 || nb < 0 || ld < nb) {
+    set_error("bad outer-product arguments");
+    return SLDG_ERR_ARG;
+  }
+  long long n = na * nb;
+  if (n == 0) return SLDG_OK;
+  k_outer<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(a, na, b, nb, out, ld);
+  SLDG_LAUNCH_CHECK("k_outer");
+  return SLDG_OK;
+}
 
 int sldg_overlap_pairs(const SldgBasis* basis, const double* fracs, int64_t n, double* A,
                        double* B, void* stream) {

@@ -184,7 +184,7 @@ class ShardedSimulation:
 
         from ._device import device, to_device_f64
         from .basis import DGBasis
-        from .driver import sample_initial, velocity_dof_coords, velocity_dof_weights
+        from .driver import sample_initial_into, velocity_dof_coords, velocity_dof_weights
         from .pencil import classify_conforming, extract_pencils
         from .tensor import build_permutation
         from .vmesh import build_mesh
@@ -223,7 +223,7 @@ class ShardedSimulation:
         n_v = len(self.vweights)
         self._F = torch.zeros((n_v, self.width), dtype=torch.float64, device=dev)
         self._G = torch.zeros_like(self._F)
-        self.f.copy_(to_device_f64(sample_initial(c, self.vcoords, self.xgrid.dof_coords[x0:x1])))
+        sample_initial_into(c, self.vcoords, self.xgrid.dof_coords[x0:x1], self.f)
         self._rho_loc = torch.empty(self.n_local * o, dtype=torch.float64, device=dev)
         self._phi = torch.empty(self.poisson.n_nodes, dtype=torch.float64, device=dev)
         self._e = torch.empty(self.xgrid.n_dofs, dtype=torch.float64, device=dev)
