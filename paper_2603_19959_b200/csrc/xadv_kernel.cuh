@@ -355,259 +355,4 @@ k_xadv(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __re
 
 }  // namespace sldg
 
-namespace sldg {
-
-// ---------------------------------------------------------------------------
-// Specialised variant for rows of CPC x (power of two <= 32) cells, CPC = 8.
-// Every row chunk (CPC*O doubles, 16-byte aligned in HBM) is fetched by one
-// lane with a cp.async.bulk (TMA engine) into the padded shared-memory slot,
-// plus a ghost copy of chunk 0 after the last chunk, so a lane's CPC+1
-// source cells never wrap.  Completion: one mbarrier per slot (transaction
-// bytes).  Row metadata (speed index, weights) is prefetched into registers
-// one iteration ahead.  For X.X the intermediate row is written back into the
-// consumed slot.  Outputs go from registers straight to HBM (16-byte stores).
-// Same arithmetic as k_xadv (bitwise-identical results and reductions).
-// ---------------------------------------------------------------------------
-struct XcGeom {
-  int lpr, rpw, cs, rs, slot, shared_dbl, per_warp, tab_dbl;
-};
-
-template <int O, int CPC>
-__host__ __device__ inline XcGeom xc_geom(int n_cells, long long n_speeds) {
-  XcGeom g;
-  g.lpr = n_cells / CPC;
-  g.rpw = 32 / g.lpr;
-  constexpr int CO = CPC * O;
-  g.cs = (CO % 2 == 0) ? ((CO / 2) | 1) * 2 : CO;     // see x_geom
-  g.rs = (g.lpr + 1) * g.cs;                         // + ghost chunk
-  g.slot = g.rpw * g.rs;
-  g.tab_dbl = (int)(n_speeds * 2 * O * O);
-  const int small = (int)((n_speeds * 5 + 7) / 8 + 1);
-  g.shared_dbl = (g.tab_dbl + n_cells * O + small + 1) & ~1;   // table, x weights, shifts
-  g.per_warp = kXNBuf * g.slot;
-  return g;
-}
-
-template <int O, int NAPPLY, bool MOM, bool RHO, int CPC>
-__global__ void __launch_bounds__(256, 1)
-k_xadv_c(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __restrict__ fout,
-         long long ld_out, long long n_rows, int n_cells, int n_speeds, XEpi epi) {
-  constexpr int CO = CPC * O;
-  static_assert(CO % 2 == 0, "vector path needs an even chunk length");
-  extern __shared__ __align__(128) double sm[];
-  const XcGeom G = xc_geom<O, CPC>(n_cells, n_speeds);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int grp = lane / G.lpr, sub = lane - grp * G.lpr;
-  const int row_len = n_cells * O;
-  double* tab = sm;
-  double* xw_s = sm + G.tab_dbl;
-  int* nsm_s = reinterpret_cast<int*>(xw_s + row_len);
-  unsigned char* id_s = reinterpret_cast<unsigned char*>(nsm_s + n_speeds);
-  double* wbase = sm + G.shared_dbl + (long long)warp * G.per_warp;
-  __shared__ __align__(8) unsigned long long full[8][kXNBuf];
-  __shared__ double mom_red[8][3];
-
-  for (int q = threadIdx.x; q < G.tab_dbl; q += blockDim.x) tab[q] = __ldg(X.mats + q);
-  for (int q = threadIdx.x; q < n_speeds; q += blockDim.x) {
-    nsm_s[q] = __ldg(X.nsm + q);
-    id_s[q] = X.ident[q];
-  }
-  if (MOM)
-    for (int q = threadIdx.x; q < row_len; q += blockDim.x) xw_s[q] = __ldg(epi.xw + q);
-  if (lane == 0) {
-    for (int k = 0; k < kXNBuf; ++k) mbar_init(&full[warp][k], 1);
-    mbar_fence_init();
-  }
-  double racc[RHO ? CO : 1];
-#pragma unroll
-  for (int q = 0; q < (RHO ? CO : 1); ++q) racc[q] = 0.0;
-  __syncthreads();
-
-  const long long ngroups = (n_rows + G.rpw - 1) / G.rpw;
-  const long long gw = (long long)blockIdx.x * nwarps + warp;
-  const long long tw = (long long)gridDim.x * nwarps;
-  double m0 = 0.0, m1 = 0.0, m2 = 0.0;
-  const int chunks = G.lpr + 1;
-
-  // bulk-copy row group rg into slot s: lane q -> (row q / chunks, chunk q % chunks)
-  auto issue = [&](long long rg, int s) {
-    double* dst = wbase + s * G.slot;
-    const long long row0 = rg * G.rpw;
-    const int nr = (int)min((long long)G.rpw, n_rows - row0);
-    if (lane == 0) mbar_expect_tx(&full[warp][s], (unsigned)(nr * chunks * CO * 8));
-    __syncwarp();
-    for (int q = lane; q < nr * chunks; q += 32) {
-      const int r = q / chunks, ch = q - r * chunks;
-      const int chs = ch < G.lpr ? ch : 0;          // ghost re-reads chunk 0
-      bulk_g2s(dst + r * G.rs + ch * G.cs, fin + (row0 + r) * ld_in + chs * CO,
-               (unsigned)(CO * 8), &full[warp][s]);
-    }
-  };
-  // per-row metadata for this lane's row of group rg
-  struct Meta {
-    int g;
-    double w, v0, v2;
-  };
-  auto fetch_meta = [&](long long rg) {
-    Meta m{0, 0.0, 0.0, 0.0};
-    const long long row = rg * G.rpw + grp;
-    if (rg < ngroups && row < n_rows) {
-      m.g = __ldg(X.row_speed + row);
-      if (MOM || RHO) m.w = __ldg(epi.w + row);
-      if (MOM) {
-        m.v0 = __ldg(epi.v0 + row);
-        m.v2 = __ldg(epi.v2 + row);
-      }
-    }
-    return m;
-  };
-
-  // one application on this lane's chunk (src row with ghost); y: CO outputs
-  auto apply = [&](const double* srow, int nsm, bool ident, const double* AB, double* y) {
-    if (ident) {
-#pragma unroll
-      for (int q = 0; q < CO; ++q) y[q] = srow[sub * G.cs + q];
-      return;
-    }
-    double a[O * O], b[O * O];
-#pragma unroll
-    for (int q = 0; q < O * O; ++q) {
-      a[q] = AB[q];
-      b[q] = AB[O * O + q];
-    }
-    int t = sub * CPC - nsm - 1;
-    if (t < 0) t += n_cells;
-    double ub[O];
-    {
-      const int off = t * O + (G.cs - CO) * (t / CPC);
-#pragma unroll
-      for (int j = 0; j < O; ++j) ub[j] = srow[off + j];
-    }
-#pragma unroll
-    for (int k = 0; k < CPC; ++k) {
-      const int tt = t + 1 + k;
-      const int off = tt * O + (G.cs - CO) * (tt / CPC);
-      double ua[O];
-#pragma unroll
-      for (int j = 0; j < O; ++j) ua[j] = srow[off + j];
-#pragma unroll
-      for (int i = 0; i < O; ++i) {
-        double sa = a[i * O] * ua[0];
-        double sb = b[i * O] * ub[0];
-#pragma unroll
-        for (int j = 1; j < O; ++j) {
-          sa = fma(a[i * O + j], ua[j], sa);
-          sb = fma(b[i * O + j], ub[j], sb);
-        }
-        y[k * O + i] = sa + sb;
-      }
-#pragma unroll
-      for (int j = 0; j < O; ++j) ub[j] = ua[j];
-    }
-  };
-
-  for (int p = 0; p < kXNBuf - 1; ++p) {
-    long long rg = gw + p * tw;
-    if (rg < ngroups) issue(rg, p);
-  }
-  Meta meta = fetch_meta(gw);
-  int it = 0;
-  for (long long rg = gw; rg < ngroups; rg += tw, ++it) {
-    const long long rn = rg + (kXNBuf - 1) * tw;
-    if (rn < ngroups) issue(rn, (it + kXNBuf - 1) % kXNBuf);
-    const Meta next = fetch_meta(rg + tw);
-    const int s = it % kXNBuf;
-    mbar_wait(&full[warp][s], (unsigned)((it / kXNBuf) & 1));
-    double* cur = wbase + s * G.slot;
-    const long long row = rg * G.rpw + grp;
-    const bool live = row < n_rows;
-    double s_mom = 0.0;
-    double y[CO];
-    const int g = meta.g;
-    const bool ident = id_s[g] != 0;
-    const int nsm = nsm_s[g];
-    const double* AB = tab + (long long)g * 2 * O * O;
-    double* srow = cur + grp * G.rs;
-    if (live) {
-      apply(srow, nsm, ident, AB, y);
-      if (MOM) {
-#pragma unroll
-        for (int q = 0; q < CO; ++q) s_mom = fma(y[q], xw_s[sub * CO + q], s_mom);
-      }
-    }
-    if (NAPPLY == 2) {
-      __syncwarp();                     // every lane has read its sources
-      if (live) {
-#pragma unroll
-        for (int q = 0; q < CO; ++q) srow[sub * G.cs + q] = y[q];
-        if (sub == 0) {
-#pragma unroll
-          for (int q = 0; q < CO; ++q) srow[G.lpr * G.cs + q] = y[q];   // ghost
-        }
-      }
-      __syncwarp();
-      if (live) apply(srow, nsm, ident, AB, y);
-    }
-    if (live) {
-      double* dst = fout + row * ld_out + sub * CO;
-#pragma unroll
-      for (int q = 0; q < CO / 2; ++q)
-        reinterpret_cast<double2*>(dst)[q] = make_double2(y[2 * q], y[2 * q + 1]);
-      if (RHO) {
-#pragma unroll
-        for (int q = 0; q < CO; ++q) racc[q] = fma(meta.w, y[q], racc[q]);
-      }
-    }
-    if (MOM) {
-      for (int o = G.lpr >> 1; o > 0; o >>= 1) s_mom += __shfl_xor_sync(0xffffffffu, s_mom, o);
-      if (live) {
-        m0 += meta.w * s_mom;
-        m1 = fma(meta.w * meta.v0, s_mom, m1);
-        m2 = fma(meta.w * meta.v2, s_mom, m2);
-      }
-    }
-    meta = next;
-    __syncwarp();                       // slot s is refilled next iteration
-  }
-  if (MOM) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int q = 0; q < G.rpw; ++q) {
-      a0 += __shfl_sync(0xffffffffu, m0, q * G.lpr);
-      a1 += __shfl_sync(0xffffffffu, m1, q * G.lpr);
-      a2 += __shfl_sync(0xffffffffu, m2, q * G.lpr);
-    }
-    if (lane == 0) {
-      mom_red[warp][0] = a0;
-      mom_red[warp][1] = a1;
-      mom_red[warp][2] = a2;
-    }
-  }
-  if (RHO) {   // per-warp column partial = sum over row groups in order -> slot 0 (dense)
-    double* part = wbase;
-    for (int q = 0; q < G.rpw; ++q) {
-      if (grp == q) {
-#pragma unroll
-        for (int k = 0; k < CO; ++k) {
-          const int off = sub * CO + k;
-          part[off] = (q == 0) ? racc[k] : part[off] + racc[k];
-        }
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  if (MOM && threadIdx.x < 3) {
-    double s = 0.0;
-    for (int q = 0; q < nwarps; ++q) s += mom_red[q][threadIdx.x];
-    epi.mom_part[blockIdx.x * 3 + threadIdx.x] = s;
-  }
-  if (RHO) {
-    for (int e = threadIdx.x; e < row_len; e += blockDim.x) {
-      double s = 0.0;
-      for (int q = 0; q < nwarps; ++q) s += sm[G.shared_dbl + (long long)q * G.per_warp + e];
-      epi.rho_part[(long long)blockIdx.x * row_len + e] = s;
-    }
-  }
-}
-
-}  // namespace sldg
+#include "xadv_c_kernel.cuh"

@@ -358,12 +358,17 @@ struct XadvGeom {
 // fused reductions are bitwise reproducible.
 // Rows of 8 x (power of two <= 32) cells with a shared-memory speed table use
 // the specialised k_xadv_c (compile-time chunk of 8 cells).
-static bool xadv_c_eligible(const sldg_xplan* X) {
+// chunk length of the specialised kernel for this plan: 8, 16, or 0 (not eligible)
+static int xadv_c_eligible(const sldg_xplan* X) {
   const long long n = X->n_cells;
-  if (X->o < 2 || X->o > 4 || n % 8 != 0) return false;
-  const long long l = n / 8;
-  if (l < 1 || l > 32 || (l & (l - 1)) != 0) return false;
-  return X->n_speeds * 2 * X->o * X->o * sizeof(double) <= 32 * 1024;
+  if (X->o < 2 || X->o > 4) return 0;
+  if (X->n_speeds * 2 * X->o * X->o * sizeof(double) > 32 * 1024) return 0;
+  for (int cpc : {8, 16}) {
+    if (n % cpc != 0) continue;
+    const long long l = n / cpc;
+    if (l >= 1 && l <= 32 && (l & (l - 1)) == 0) return cpc;
+  }
+  return 0;
 }
 
 static XadvGeom xadv_geom(const sldg_xplan* X, int napply, bool rho, bool allow_c = true) {
@@ -374,13 +379,18 @@ static XadvGeom xadv_geom(const sldg_xplan* X, int napply, bool rho, bool allow_
   XGeom G = x_geom((int)X->n_cells, X->o, X->n_speeds, g.tab_smem, 1 << 30);
   g.cpcm = G.cpc <= 8 ? 8 : (G.cpc <= 16 ? 16 : 0);
   int shared_dbl = G.shared_dbl, per_warp = G.per_warp, rpw = G.rpw;
-  if (allow_c && xadv_c_eligible(X)) {
-    g.cpcm = -8;   // marks the specialised kernel
+  const int cpc = allow_c ? xadv_c_eligible(X) : 0;
+  if (cpc) {
+    g.cpcm = -cpc;   // marks the specialised kernel
     XcGeom C;
-    switch (X->o) {
-      case 2: C = xc_geom<2, 8>((int)X->n_cells, X->n_speeds); break;
-      case 3: C = xc_geom<3, 8>((int)X->n_cells, X->n_speeds); break;
-      default: C = xc_geom<4, 8>((int)X->n_cells, X->n_speeds); break;
+    const int n = (int)X->n_cells;
+    switch (X->o * 100 + cpc) {
+      case 208: C = xc_geom<2, 8>(n, X->n_speeds); break;
+      case 308: C = xc_geom<3, 8>(n, X->n_speeds); break;
+      case 408: C = xc_geom<4, 8>(n, X->n_speeds); break;
+      case 216: C = xc_geom<2, 16>(n, X->n_speeds); break;
+      case 316: C = xc_geom<3, 16>(n, X->n_speeds); break;
+      default: C = xc_geom<4, 16>(n, X->n_speeds); break;
     }
     shared_dbl = C.shared_dbl;
     per_warp = C.per_warp;
@@ -414,8 +424,8 @@ template <int O, int NAPPLY, bool MOM, bool RHO>
 static int launch_xadv_t(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
                          long long ld_out, const XEpi& epi, const XadvGeom& g, bool vec,
                          cudaStream_t st) {
-  if (g.cpcm == -8) {
-    auto kc = k_xadv_c<O, NAPPLY, MOM, RHO, 8>;
+  if (g.cpcm < 0) {
+    auto kc = g.cpcm == -8 ? k_xadv_c<O, NAPPLY, MOM, RHO, 8> : k_xadv_c<O, NAPPLY, MOM, RHO, 16>;
     SLDG_CUDA_TRY(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)std::max<size_t>(g.smem, 48 * 1024)));
     kc<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
