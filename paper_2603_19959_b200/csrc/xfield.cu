@@ -363,7 +363,7 @@ static int xadv_c_eligible(const sldg_xplan* X) {
   const long long n = X->n_cells;
   if (X->o < 2 || X->o > 4) return 0;
   if (X->n_speeds * 2 * X->o * X->o * sizeof(double) > 32 * 1024) return 0;
-  for (int cpc : {8, 16}) {
+  for (int cpc : {8}) {   // the 16-cell variant measured slower than k_xadv (r01 profiles)
     if (n % cpc != 0) continue;
     const long long l = n / cpc;
     if (l >= 1 && l <= 32 && (l & (l - 1)) == 0) return cpc;
