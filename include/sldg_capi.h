@@ -179,6 +179,21 @@ int sldg_poisson_efield(const sldg_poisson* p, const double* phi, double* e, voi
 /* out2 = [max|E|, 0.5 * w.E^2]  (driver.py:220-229, xfield.py:192-195) */
 int sldg_field_diag(const sldg_poisson* p, const double* e, double* out2, void* stream);
 
+/* ------------------------------------------------ fused Strang step (one HBM pass) */
+/* Steady-state step of Simulation.advance (csrc/step_fused.cu): from the state after the
+ * leading half x-step, f_out = X(X(V(f_in; speeds = E, dt))) with the moments of
+ * X(V(f_in)) (the step's diagnostics) in mom_out3 and rho of f_out in rho_out (the next
+ * step's field source).  Replaces advect_velocity + advect_x + moments + advect_x +
+ * compute_rho (vsweep.py:413-441, xfield.py:91-109, driver.py:139-146) in one pass.
+ * _query returns SLDG_ERR_UNSUPPORTED (with the reason) for plans it does not cover. */
+int sldg_step_fused_query(const sldg_vplan* vplan, const sldg_xplan* xplan, int64_t n_cols,
+                          int64_t ld, size_t* scratch_bytes);
+int sldg_step_fused(const sldg_vplan* vplan, const sldg_xplan* xplan, const double* f_in,
+                    double* f_out, int64_t ld, int64_t n_cols, const double* speeds, double dt,
+                    int32_t bc, const double* w, const double* v0, const double* v2,
+                    const double* xw, double* mom_out3, double* rho_out, void* scratch,
+                    void* stream);
+
 /* ---------------------------------------------------------------- misc */
 /* out[i*ld + j] = a[i] * b[j]: the separable initial condition sampled on the
  * device (sample_initial, driver.py:132-136), bit-identical to numpy's product. */

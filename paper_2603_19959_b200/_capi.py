@@ -69,6 +69,12 @@ _SIGS = {
     "sldg_version": (C.c_int, []),
     "sldg_last_error": (C.c_char_p, []),
     "sldg_launch_count": (C.c_int64, []),
+    "sldg_step_fused_query": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                        C.POINTER(C.c_size_t)]),
+    "sldg_step_fused": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                  C.c_int64, C.c_void_p, C.c_double, C.c_int32, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p]),
     "sldg_outer": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                              C.c_int64, C.c_void_p]),
     "sldg_overlap_pairs": (C.c_int, [C.POINTER(SldgBasis), C.c_void_p, C.c_int64, C.c_void_p,

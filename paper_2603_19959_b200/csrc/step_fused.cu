@@ -1,0 +1,471 @@
+// step_fused.cu -- one HBM pass per Strang step: v-sweep + trailing half x-step
+// (+ moments) + next leading half x-step (+ rho), fused per line-group tile.
+//
+// In Simulation.advance() the state between kernels is f' = X(f) (after the
+// leading half x-step).  The reference step (driver.py:231-240) continues with
+// field solve -> advect_velocity (vsweep.py:413-441) -> advect_x
+// (xfield.py:91-104) -> diagnostics (driver.py:220-229, moments 139-146), and
+// the next step starts with advect_x and compute_rho (xfield.py:107-109).
+// This kernel performs, for one pencil and a group of LG lines of its cells:
+//   V  : whole-pencil fast path (sweep_pencil, vsweep.py:197-200) from a TMA
+//        bulk-copy ring of cell tiles (as k_sweep_stream), into shared memory;
+//   X1 : trailing half x-step on the tile's rows (they are complete rows:
+//        the tile spans all x columns), moments of the result accumulated;
+//   X2 : leading half x-step of the next step, rho of the result accumulated,
+//        result stored to HBM.
+// Every coefficient is read once and written once per step: 16 B/DOF instead
+// of 32 B/DOF for the separate sweep and X.X passes.  Arithmetic per output is
+// the same as in k_sweep_stream / k_xadv (same operands, same order).
+//
+// Thread mappings: V phase thread = x column (its A, B for the pencil's level
+// in registers); X phases thread = (velocity node i_v, x cell): all rows of a
+// tile with the same i_v share one v_x, hence one x-shift and one A, B pair.
+// Shared-memory rows carry ghost cells on both sides so periodic x reads never
+// wrap (writers duplicate the edge cells into the ghosts).
+//
+// Eligible: dim 3, direction 0, every pencil whole-pencil-fast, no weighted
+// (1/n_c) entries, tile rows span the whole row (ld == n_cols).  Otherwise the
+// host falls back to the separate passes.
+#include <algorithm>
+#include <string>
+
+#include "plans.cuh"
+#include "sldg_common.cuh"
+#include "tma_util.cuh"
+
+namespace sldg {
+
+static __global__ void k_fold_cols(const double* __restrict__ part, long long n_parts,
+                                   long long n_cols, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (c >= n_cols) return;
+  double s = 0.0;
+  for (long long k = lane; k < n_parts; k += 32) s += part[k * n_cols + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[c] = s;
+}
+
+static __global__ void k_fold3(const double* __restrict__ part, long long n, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w >= 3) return;
+  double s = 0.0;
+  for (long long k = lane; k < n; k += 32) s += part[k * 3 + w];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[w] = s;
+}
+
+constexpr int kFRing = 4;
+
+struct FusedArgs {
+  const double* w;
+  const double* v0;
+  const double* v2;
+  const double* xw;
+  double* mom_part;   // [grid][3]
+  double* rho_part;   // [grid][n_cols]
+};
+
+template <int OV, int OX>
+__global__ void __launch_bounds__(384, 1)
+k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout,
+             int n_cols, int n_xc, const double* __restrict__ speeds, int bc,
+             const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats, int lg,
+             int n_lg, int hl, int hr, int gl, int rw, int n_speeds, FusedArgs fa) {
+  constexpr int XM = 2 * OX * OX;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) unsigned long long full[kFRing];
+  __shared__ int s_nsmin, s_nsmax;
+
+  const int R = lg * OV;                        // rows per tile
+  const int tile = R * n_cols;                  // doubles per ring slot
+  double* ring = sm;
+  double* stA = ring + kFRing * tile;
+  double* stB = stA + R * rw;
+  double* xtab = stB + R * rw;                  // n_speeds x (A|B) for the x shift
+  double* meta = xtab + (long long)n_speeds * XM;   // [2][3][R]: w, w*v0, w*v2 per tile row
+  int* xns = reinterpret_cast<int*>(meta + 6 * R);
+  unsigned char* xid = reinterpret_cast<unsigned char*>(xns + n_speeds);
+
+  const long long wp = blockIdx.x / n_lg;
+  const int t0 = (int)(blockIdx.x - wp * n_lg) * lg;   // first line of the group
+  const long long q = P.walk_pencils[wp];
+  const long long off = P.p_off[q];
+  const int n = P.p_n[q];
+  const int lev = P.e_level[off];
+  const int tid = threadIdx.x;
+
+  for (int k = tid; k < n_speeds * XM; k += blockDim.x) xtab[k] = __ldg(X.mats + k);
+  for (int k = tid; k < n_speeds; k += blockDim.x) {
+    xns[k] = (int)X.ns[k];
+    xid[k] = X.ident[k];
+  }
+  if (tid == 0) {
+    s_nsmin = 1 << 30;
+    s_nsmax = -(1 << 30);
+    for (int k = 0; k < kFRing; ++k) mbar_init(&full[k], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  // ---- V-phase state: thread = column
+  const bool colv = tid < n_cols;
+  const int c = tid;
+  const double speed = colv ? __ldg(speeds + c) : 0.0;
+  const long long nsv = colv ? lm_ns[(long long)lev * n_cols + c] : 0;
+  if (colv && speed != 0.0) {
+    const int nsi = (int)max(min(nsv, (long long)(1 << 29)), -(long long)(1 << 29));
+    atomicMin(&s_nsmin, nsi);
+    atomicMax(&s_nsmax, nsi);
+  }
+  double Av[OV * OV], Bv[OV * OV];
+  if (colv) load_pair<OV>(lm_mats, lev, n_cols, c, Av, Bv);
+  const int cxc = colv ? c / OX : 0;
+  const bool ghostL = colv && cxc >= n_xc - hl;   // column also feeds the left ghost
+  const bool ghostR = colv && cxc < hr;           // ... and/or the right ghost
+  __syncthreads();
+  const bool streamable = (s_nsmin >= -1 && s_nsmax <= 0) || (s_nsmin > s_nsmax);
+  const bool per = (bc == SLDG_BC_PERIODIC);
+
+  // ---- X-phase state: thread = (iv, x cell)
+  const bool xv = tid < OV * n_xc;
+  const int iv = xv ? tid / n_xc : 0;
+  const int cx = xv ? tid - iv * n_xc : 0;
+  const bool xghL = xv && cx >= n_xc - hl, xghR = xv && cx < hr;
+  double m0a[OX], m1a[OX], m2a[OX], rha[OX];
+#pragma unroll
+  for (int k = 0; k < OX; ++k) m0a[k] = m1a[k] = m2a[k] = rha[k] = 0.0;
+
+  // per-cell x metadata, prefetched one cell ahead: thread q < 3R loads one of
+  // (w, w*v0, w*v2) of one tile row into a register, parks it in the meta buffer
+  auto cell_row0 = [&](int s) { return P.e_row0[off + s] + (long long)t0 * OV; };
+  auto fetch_meta = [&](int s) -> double {
+    if (tid >= 3 * R || s >= n) return 0.0;
+    const int kind = tid / R, r = tid - kind * R;
+    const long long row = cell_row0(s) + r;
+    const double wr = __ldg(fa.w + row);
+    return kind == 0 ? wr : wr * __ldg((kind == 1 ? fa.v0 : fa.v2) + row);
+  };
+  auto fetch_g = [&](int s) -> int {
+    return (xv && s < n) ? __ldg(X.row_speed + cell_row0(s) + iv) : 0;
+  };
+  {
+    const double m = fetch_meta(0);
+    if (tid < 3 * R) meta[tid] = m;
+  }
+  int g_cur = fetch_g(0);
+  __syncthreads();
+
+  // ---- ring of cell tiles (as k_sweep_stream)
+  const int v0c = per ? -1 : 0;
+  const int n_load = per ? n + 2 : n;
+  auto issue = [&](int k) {
+    const int v = v0c + k;
+    const int cell = v < 0 ? n - 1 : (v >= n ? 0 : v);
+    unsigned long long* bar = &full[k % kFRing];
+    mbar_expect_tx(bar, (unsigned)(tile * 8));
+    bulk_g2s(ring + (k % kFRing) * tile, fin + cell_row0(cell) * n_cols, (unsigned)(tile * 8), bar);
+  };
+  if (streamable && tid == 0)
+    for (int k = 0; k < min(3, n_load); ++k) issue(k);
+
+  auto put = [&](double* st, int r, int col, double y, bool gL, bool gR) {
+    double* rowp = st + r * rw + gl;
+    rowp[col] = y;
+    if (gL) rowp[col - n_cols] = y;
+    if (gR) rowp[col + n_cols] = y;
+  };
+
+  for (int s = 0; s < n; ++s) {
+    const double meta_nxt = fetch_meta(s + 1);
+    const int g_nxt = fetch_g(s + 1);
+    const double* mcur = meta + (s & 1) * 3 * R;
+    // ===================== V: pencil sweep of cell s -> stA
+    if (streamable) {
+      const int kn = s + 2 - v0c;
+      if (tid == 0 && kn < n_load && kn >= 3) issue(kn);
+      const int klo = max(s - 1 - v0c, 0), khi = min(s + 1 - v0c, n_load - 1);
+      for (int k = klo; k <= khi; ++k) mbar_wait(&full[k % kFRing], (unsigned)((k / kFRing) & 1));
+    }
+    if (colv) {
+      if (speed == 0.0) {
+        const double* me = streamable ? ring + ((s - v0c) % kFRing) * tile + c
+                                      : fin + cell_row0(s) * n_cols + c;
+        for (int r = 0; r < R; ++r) put(stA, r, c, me[r * n_cols], ghostL, ghostR);
+      } else {
+        const int va_cell = s - (int)nsv, vb_cell = s - (int)nsv - 1;
+        bool va = true, vb = true;
+        const double *sa, *sb;
+        if (streamable) {
+          va = per || (va_cell >= 0 && va_cell < n);
+          vb = per || (vb_cell >= 0 && vb_cell < n);
+          sa = ring + ((va ? va_cell : s) - v0c) % kFRing * tile + c;
+          sb = ring + ((vb ? vb_cell : s) - v0c) % kFRing * tile + c;
+        } else {
+          long long qa = va_cell, qb = vb_cell;
+          if (per) {
+            qa = pymod(qa, n);
+            qb = pymod(qb, n);
+          } else {
+            va = qa >= 0 && qa < n;
+            vb = qb >= 0 && qb < n;
+          }
+          sa = fin + cell_row0(va ? (int)qa : s) * n_cols + c;
+          sb = fin + cell_row0(vb ? (int)qb : s) * n_cols + c;
+        }
+        for (int t = 0; t < lg; ++t) {
+          double ua[OV], ub[OV], y[OV];
+#pragma unroll
+          for (int i = 0; i < OV; ++i) {
+            ua[i] = va ? sa[(t * OV + i) * n_cols] : 0.0;
+            ub[i] = vb ? sb[(t * OV + i) * n_cols] : 0.0;
+          }
+          two_cell<OV>(Av, Bv, ua, ub, va, vb, y);
+#pragma unroll
+          for (int i = 0; i < OV; ++i) put(stA, t * OV + i, c, y[i], ghostL, ghostR);
+        }
+      }
+    }
+    __syncthreads();
+    // ===================== X1 (trailing half step): stA -> stB, moments
+    const bool ident = xid[g_cur] != 0;
+    const int nx = xns[g_cur];
+    const double* AB = xtab + (long long)g_cur * XM;
+    auto xapply = [&](const double* srow, double* y) {
+      if (ident) {
+#pragma unroll
+        for (int k = 0; k < OX; ++k) y[k] = srow[cx * OX + k];
+        return;
+      }
+      const double* ua = srow + (cx - nx) * OX;
+      const double* ub = ua - OX;
+#pragma unroll
+      for (int k = 0; k < OX; ++k) {
+        double sa = AB[k * OX] * ua[0];
+        double sb = AB[OX * OX + k * OX] * ub[0];
+#pragma unroll
+        for (int j = 1; j < OX; ++j) {
+          sa = fma(AB[k * OX + j], ua[j], sa);
+          sb = fma(AB[OX * OX + k * OX + j], ub[j], sb);
+        }
+        y[k] = sa + sb;
+      }
+    };
+    if (xv) {
+      for (int t = 0; t < lg; ++t) {
+        const int r = t * OV + iv;
+        double y[OX];
+        xapply(stA + r * rw + gl, y);
+        const double wr = mcur[r], wv0 = mcur[R + r], wv2 = mcur[2 * R + r];
+#pragma unroll
+        for (int k = 0; k < OX; ++k) {
+          put(stB, r, cx * OX + k, y[k], xghL, xghR);
+          m0a[k] = fma(wr, y[k], m0a[k]);
+          m1a[k] = fma(wv0, y[k], m1a[k]);
+          m2a[k] = fma(wv2, y[k], m2a[k]);
+        }
+      }
+    }
+    __syncthreads();
+    // ===================== X2 (next step's leading half): stB -> HBM, rho
+    if (xv) {
+      const long long r0 = cell_row0(s);
+      for (int t = 0; t < lg; ++t) {
+        const int r = t * OV + iv;
+        double y[OX];
+        xapply(stB + r * rw + gl, y);
+        double* dst = fout + (r0 + r) * n_cols + cx * OX;
+#pragma unroll
+        for (int k = 0; k < OX; ++k) {
+          dst[k] = y[k];
+          rha[k] = fma(mcur[r], y[k], rha[k]);
+        }
+      }
+    }
+    g_cur = g_nxt;
+    if (tid < 3 * R) meta[((s + 1) & 1) * 3 * R + tid] = meta_nxt;
+    __syncthreads();   // ring slot of cell s-1, stA/stB and the meta buffer are reused next
+  }
+
+  // ---- CTA partials: rho per column (over i_v in order), moments contracted with xw
+  double* red = stA;   // reuse: OV x n_cols, then 3 x blockDim
+  if (xv) {
+#pragma unroll
+    for (int k = 0; k < OX; ++k) red[iv * n_cols + cx * OX + k] = rha[k];
+  }
+  __syncthreads();
+  if (colv) {
+    double s = 0.0;
+    for (int k = 0; k < OV; ++k) s += red[k * n_cols + c];
+    fa.rho_part[(long long)blockIdx.x * n_cols + c] = s;
+  }
+  __syncthreads();
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  if (xv) {
+#pragma unroll
+    for (int k = 0; k < OX; ++k) {
+      const double xwk = __ldg(fa.xw + cx * OX + k);
+      s0 = fma(xwk, m0a[k], s0);
+      s1 = fma(xwk, m1a[k], s1);
+      s2 = fma(xwk, m2a[k], s2);
+    }
+  }
+  red[tid] = s0;
+  red[blockDim.x + tid] = s1;
+  red[2 * blockDim.x + tid] = s2;
+  __syncthreads();
+  if (tid < 3) {
+    double s = 0.0;
+    for (int k = 0; k < (int)blockDim.x; ++k) s += red[tid * blockDim.x + k];
+    fa.mom_part[blockIdx.x * 3 + tid] = s;
+  }
+}
+
+struct FusedGeom {
+  bool ok;
+  int lg, n_lg, gl, rw, threads;
+  size_t smem;
+  long long grid;
+  std::string why;
+};
+
+static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long long n_cols,
+                            long long ld) {
+  FusedGeom g{};
+  g.ok = false;
+  const int OV = vp->o, OX = xp->o;
+  auto no = [&](const char* w) {
+    g.why = w;
+    return g;
+  };
+  if (vp->dim != 3 || vp->direction != 0) return no("fused step: dim 3, direction 0 only");
+  if (vp->n_gen != 0 || vp->n_slots != 0) return no("fused step: AMR boundary / weighted entries");
+  if (ld != n_cols || n_cols != xp->n_cells * OX) return no("fused step: whole rows only");
+  if (OV < 2 || OV > 4 || OX < 2 || OX > 4) return no("fused step: degrees 1..3");
+  const long long threads = std::max<long long>(n_cols, OV * xp->n_cells);
+  if (threads > 384) return no("fused step: rows wider than 384 columns");
+  const int hl = (int)xp->halo_l, hr = (int)xp->halo_r;
+  if (hl > xp->n_cells || hr > xp->n_cells) return no("fused step: shift wider than the row");
+  g.gl = ((hl * OX) + 1) & ~1;
+  g.rw = g.gl + (int)n_cols + (((hr * OX) + 1) & ~1);
+  const size_t fixed = sizeof(double) * (size_t)xp->n_speeds * 2 * OX * OX + 5 * xp->n_speeds + 64 +
+                       sizeof(double) * 6 * 8 * OV;
+  const size_t budget = 227 * 1024 - 1024;
+  g.lg = 0;
+  for (int lg = std::min(8, OV * OV); lg >= 1; --lg) {
+    if ((OV * OV) % lg) continue;
+    const size_t R = (size_t)lg * OV;
+    const size_t smem = sizeof(double) * (kFRing * R * n_cols + 2 * R * g.rw) + fixed;
+    const size_t red = sizeof(double) * std::max<size_t>(OV * n_cols, 3 * threads);
+    if (smem <= budget && sizeof(double) * 2 * R * g.rw >= red) {
+      // prefer two CTAs per SM when possible
+      if (2 * smem <= budget || g.lg == 0) {
+        g.lg = lg;
+        g.smem = smem;
+        if (2 * smem <= budget) break;
+      }
+    }
+  }
+  if (g.lg == 0) return no("fused step: tile does not fit in shared memory");
+  g.n_lg = OV * OV / g.lg;
+  g.threads = (int)((threads + 31) / 32 * 32);
+  g.grid = vp->n_walk * g.n_lg;
+  g.ok = true;
+  return g;
+}
+
+template <int OV, int OX>
+static int launch_fused(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
+                        const double* fin, double* fout, long long n_cols, const double* speeds,
+                        int bc, const long long* lm_ns, const double* lm_mats,
+                        const FusedArgs& fa, cudaStream_t st) {
+  auto k = k_step_fused<OV, OX>;
+  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  k<<<(unsigned)g.grid, g.threads, g.smem, st>>>(
+      vp->dev, xp->dev, fin, fout, (int)n_cols, (int)xp->n_cells, speeds, bc, lm_ns, lm_mats,
+      g.lg, g.n_lg, (int)xp->halo_l, (int)xp->halo_r, g.gl, g.rw, (int)xp->n_speeds, fa);
+  SLDG_LAUNCH_CHECK("k_step_fused");
+  return SLDG_OK;
+}
+
+static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+}  // namespace sldg
+
+using namespace sldg;
+
+extern "C" {
+
+int sldg_step_fused_query(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_cols, int64_t ld,
+                          size_t* scratch_bytes) {
+  if (!vp || !xp || !scratch_bytes) {
+    set_error("null argument");
+    return SLDG_ERR_ARG;
+  }
+  FusedGeom g = fused_geom(vp, xp, n_cols, ld);
+  if (!g.ok) {
+    set_error(g.why);
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  const size_t lm = al256(sizeof(long long) * vp->dev.n_levels * n_cols) +
+                    al256(sizeof(double) * vp->dev.n_levels * n_cols) +
+                    al256(sizeof(double) * vp->dev.n_levels * 2 * vp->o * vp->o * n_cols);
+  *scratch_bytes = lm + al256(sizeof(double) * g.grid * 3) + al256(sizeof(double) * g.grid * n_cols);
+  return SLDG_OK;
+}
+
+int sldg_step_fused(const sldg_vplan* vp, const sldg_xplan* xp, const double* fin, double* fout,
+                    int64_t ld, int64_t n_cols, const double* speeds, double dt, int32_t bc,
+                    const double* w, const double* v0, const double* v2, const double* xw,
+                    double* mom_out3, double* rho_out, void* scratch, void* stream) {
+  if (!vp || !xp || !fin || !fout || fin == fout || !speeds || !w || !v0 || !v2 || !xw ||
+      !mom_out3 || !rho_out || !scratch || !(dt > 0.0) ||
+      (bc != SLDG_BC_PERIODIC && bc != SLDG_BC_ABSORBING)) {
+    set_error("bad sldg_step_fused arguments");
+    return SLDG_ERR_ARG;
+  }
+  FusedGeom g = fused_geom(vp, xp, n_cols, ld);
+  if (!g.ok) {
+    set_error(g.why);
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  if ((((unsigned long long)fin) & 15) != 0 || n_cols % 2 != 0) {
+    set_error("fused step: 16-byte aligned rows required");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned char* sb = (unsigned char*)scratch;
+  long long* lm_ns = (long long*)sb;
+  size_t o1 = al256(sizeof(long long) * vp->dev.n_levels * n_cols);
+  double* lm_frac = (double*)(sb + o1);
+  size_t o2 = o1 + al256(sizeof(double) * vp->dev.n_levels * n_cols);
+  double* lm_mats = (double*)(sb + o2);
+  size_t o3 = o2 + al256(sizeof(double) * vp->dev.n_levels * 2 * vp->o * vp->o * n_cols);
+  double* mom_part = (double*)(sb + o3);
+  size_t o4 = o3 + al256(sizeof(double) * g.grid * 3);
+  double* rho_part = (double*)(sb + o4);
+  int rc = sldg_level_matrices(vp, speeds, n_cols, dt, (int64_t*)lm_ns, lm_frac, lm_mats, stream);
+  if (rc) return rc;
+  FusedArgs fa{w, v0, v2, xw, mom_part, rho_part};
+  rc = SLDG_ERR_UNSUPPORTED;
+  switch (vp->o * 10 + xp->o) {
+#define CASE(A, B)                                                                          \
+  case A * 10 + B:                                                                          \
+    rc = launch_fused<A, B>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st); \
+    break;
+    CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(4, 2) CASE(4, 3)
+    CASE(4, 4)
+#undef CASE
+  }
+  if (rc) return rc;
+  k_fold3<<<1, 96, 0, st>>>(mom_part, g.grid, mom_out3);
+  SLDG_LAUNCH_CHECK("k_fold3");
+  k_fold_cols<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>(rho_part, g.grid, n_cols,
+                                                                      rho_out);
+  SLDG_LAUNCH_CHECK("k_fold_cols");
+  return SLDG_OK;
+}
+
+}  // extern "C"

@@ -102,7 +102,7 @@ template <int O, int NAPPLY, bool MOM, bool RHO, int CPCM>
 __global__ void __launch_bounds__(256, 1)
 k_xadv(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* __restrict__ fout,
        long long ld_out, long long n_rows, int n_cells, int n_speeds, int tab_smem, XEpi epi) {
-  extern __shared__ __align__(16) double sm[];
+  extern __shared__ __align__(128) double sm[];
   const XGeom G = x_geom(n_cells, O, n_speeds, tab_smem != 0, CPCM);
   const int row_len = n_cells * O;
   const int cpc_o = G.cpc * O;

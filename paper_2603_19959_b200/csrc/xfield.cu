@@ -12,39 +12,7 @@
 #include <vector>
 
 #include "sldg_common.cuh"
-
-namespace sldg {
-
-struct XPlanDev {
-  const long long* ns;     // per unique speed: integer shift
-  const unsigned char* ident;  // per unique speed: n == 0 && alpha == 0
-  const double* mats;      // per unique speed: A (o*o) then B (o*o)
-  const int* row_speed;    // per row
-  const int* nsm;          // per unique speed: n_shift mod n_cells (periodic rows)
-};
-
-}  // namespace sldg
-
-struct sldg_xplan {
-  sldg::DevBasis basis;
-  sldg::XPlanDev dev;
-  int o;
-  long long n_cells, n_rows, n_speeds;
-  long long halo_l, halo_r;
-  double h, dt;
-  void* block;
-};
-
-struct sldg_poisson {
-  int p, o;
-  long long n_cells, n_nodes, n_dofs;
-  double h, length;
-  double* xw;      // dof weights
-  double* diff;    // o*o
-  double* green;   // n_nodes^2
-  double* work;    // b (n_nodes) + scalars
-  void* block;
-};
+#include "plans.cuh"
 
 namespace sldg {
 

@@ -380,3 +380,39 @@ def test_sharded_world1_matches_simulation():
     for x, y in zip(ra, rb):
         assert abs(x.m0 - y.m0) <= 1e-13 * abs(x.m0)
         assert abs(x.e_max - y.e_max) <= 1e-11 * abs(x.e_max)
+
+
+FUSED_CASES = [dict(dim=3, n_base=8, levels=0, degree=2, n_x=32),
+               dict(dim=3, n_base=16, levels=0, degree=1, n_x=16),
+               dict(dim=3, n_base=6, levels=0, degree=3, n_x=24, bc="periodic"),
+               dict(dim=3, n_base=8, levels=0, degree=2, n_x=64, degree_x=1)]
+
+
+@pytest.mark.parametrize("kw", FUSED_CASES)
+def test_fused_step_matches_unfused_and_oracle(kw):
+    a = sv.Simulation(sv.SimConfig(**kw, n_steps=4))
+    assert a.fused_step_supported(), "uniform mesh must take the one-pass step"
+    b = sv.Simulation(sv.SimConfig(**kw, n_steps=4))
+    b._fused_ok = False
+    ta = a.advance(4).cpu().numpy()
+    tb = b.advance(4).cpu().numpy()
+    fa, fb = a.f.cpu().numpy(), b.f.cpu().numpy()
+    assert np.abs(fa - fb).max() <= 1e-13 * np.abs(fb).max()
+    np.testing.assert_allclose(ta[:, 2:], tb[:, 2:], rtol=1e-13, atol=1e-13 * abs(tb[0, 2]))
+    np.testing.assert_allclose(ta[:, :2], tb[:, :2], rtol=1e-10)
+    ref = so.Sim(**kw)
+    recs = [ref.step() for _ in range(4)]
+    assert np.abs(fa - ref.f).max() <= 1e-12 * np.abs(ref.f).max()
+    for row, r in zip(ta, recs):
+        assert abs(row[2] - r["m0"]) <= 1e-12 * abs(r["m0"])
+        assert abs(row[0] - r["e_max"]) <= 1e-10 * recs[0]["e_max"]
+
+
+def test_run_uses_fused_step_and_matches_step_loop():
+    cfg = sv.SimConfig(dim=3, n_base=8, levels=0, degree=2, n_x=32, n_steps=5)
+    res = sv.run(cfg)
+    sim = sv.Simulation(cfg)
+    recs = [sim.diagnostics(sim.field_solve())] + [sim.step() for _ in range(5)]
+    for x, y in zip(res.records, recs):
+        assert abs(x.m0 - y.m0) <= 1e-13 * abs(y.m0)
+        assert abs(x.e_max - y.e_max) <= 1e-10 * abs(recs[0].e_max)
