@@ -171,18 +171,12 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   if (streamable && tid == 0)
     for (int k = 0; k < min(3, n_load); ++k) issue(k);
 
-  auto put = [&](double* st, int r, int col, double y, bool gL, bool gR) {
-    double* rowp = st + r * rw + gl;
-    rowp[col] = y;
-    if (gL) rowp[col - n_cols] = y;
-    if (gR) rowp[col + n_cols] = y;
-  };
-
   for (int s = 0; s < n; ++s) {
     const double meta_nxt = fetch_meta(s + 1);
     const int g_nxt = fetch_g(s + 1);
     const double* mcur = meta + (s & 1) * 3 * R;
-    // ===================== V: pencil sweep of cell s -> stA
+    const long long r0 = cell_row0(s);
+    // ===================== V: pencil sweep of cell s -> stA (rows of R, stride rw)
     if (streamable) {
       const int kn = s + 2 - v0c;
       if (tid == 0 && kn < n_load && kn >= 3) issue(kn);
@@ -190,10 +184,11 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       for (int k = klo; k <= khi; ++k) mbar_wait(&full[k % kFRing], (unsigned)((k / kFRing) & 1));
     }
     if (colv) {
+      double* out = stA + c;
       if (speed == 0.0) {
         const double* me = streamable ? ring + ((s - v0c) % kFRing) * tile + c
-                                      : fin + cell_row0(s) * n_cols + c;
-        for (int r = 0; r < R; ++r) put(stA, r, c, me[r * n_cols], ghostL, ghostR);
+                                      : fin + r0 * n_cols + c;
+        for (int r = 0; r < R; ++r) out[r * rw] = me[r * n_cols];
       } else {
         const int va_cell = s - (int)nsv, vb_cell = s - (int)nsv - 1;
         bool va = true, vb = true;
@@ -219,49 +214,72 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
           double ua[OV], ub[OV], y[OV];
 #pragma unroll
           for (int i = 0; i < OV; ++i) {
-            ua[i] = va ? sa[(t * OV + i) * n_cols] : 0.0;
-            ub[i] = vb ? sb[(t * OV + i) * n_cols] : 0.0;
+            ua[i] = va ? sa[i * n_cols] : 0.0;
+            ub[i] = vb ? sb[i * n_cols] : 0.0;
           }
           two_cell<OV>(Av, Bv, ua, ub, va, vb, y);
 #pragma unroll
-          for (int i = 0; i < OV; ++i) put(stA, t * OV + i, c, y[i], ghostL, ghostR);
+          for (int i = 0; i < OV; ++i) out[i * rw] = y[i];
+          sa += OV * n_cols;
+          sb += OV * n_cols;
+          out += OV * rw;
         }
       }
     }
-    __syncthreads();
-    // ===================== X1 (trailing half step): stA -> stB, moments
+    // x shift of this thread's rows for cell s: matrices to registers, wrapped sources
     const bool ident = xid[g_cur] != 0;
-    const int nx = xns[g_cur];
-    const double* AB = xtab + (long long)g_cur * XM;
+    double xa[OX * OX], xb[OX * OX];
+    int ia = 0, ib = 0;
+    if (xv) {
+      const double* AB = xtab + (long long)g_cur * XM;
+#pragma unroll
+      for (int k = 0; k < OX * OX; ++k) {
+        xa[k] = AB[k];
+        xb[k] = AB[OX * OX + k];
+      }
+      ia = cx - xns[g_cur];
+      ia = ia < 0 ? ia + n_xc : (ia >= n_xc ? ia - n_xc : ia);
+      ib = ia == 0 ? n_xc - 1 : ia - 1;
+      if (ident) ia = cx;
+      ia *= OX;
+      ib *= OX;
+    }
     auto xapply = [&](const double* srow, double* y) {
       if (ident) {
 #pragma unroll
-        for (int k = 0; k < OX; ++k) y[k] = srow[cx * OX + k];
+        for (int k = 0; k < OX; ++k) y[k] = srow[ia + k];
         return;
       }
-      const double* ua = srow + (cx - nx) * OX;
-      const double* ub = ua - OX;
+      double ua[OX], ub[OX];
+#pragma unroll
+      for (int j = 0; j < OX; ++j) {
+        ua[j] = srow[ia + j];
+        ub[j] = srow[ib + j];
+      }
 #pragma unroll
       for (int k = 0; k < OX; ++k) {
-        double sa = AB[k * OX] * ua[0];
-        double sb = AB[OX * OX + k * OX] * ub[0];
+        double sa = xa[k * OX] * ua[0];
+        double sb = xb[k * OX] * ub[0];
 #pragma unroll
         for (int j = 1; j < OX; ++j) {
-          sa = fma(AB[k * OX + j], ua[j], sa);
-          sb = fma(AB[OX * OX + k * OX + j], ub[j], sb);
+          sa = fma(xa[k * OX + j], ua[j], sa);
+          sb = fma(xb[k * OX + j], ub[j], sb);
         }
         y[k] = sa + sb;
       }
     };
+    __syncthreads();
+    // ===================== X1 (trailing half step): stA -> stB, moments
     if (xv) {
       for (int t = 0; t < lg; ++t) {
         const int r = t * OV + iv;
         double y[OX];
-        xapply(stA + r * rw + gl, y);
+        xapply(stA + r * rw, y);
         const double wr = mcur[r], wv0 = mcur[R + r], wv2 = mcur[2 * R + r];
+        double* o = stB + r * rw + cx * OX;
 #pragma unroll
         for (int k = 0; k < OX; ++k) {
-          put(stB, r, cx * OX + k, y[k], xghL, xghR);
+          o[k] = y[k];
           m0a[k] = fma(wr, y[k], m0a[k]);
           m1a[k] = fma(wv0, y[k], m1a[k]);
           m2a[k] = fma(wv2, y[k], m2a[k]);
@@ -271,17 +289,18 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     __syncthreads();
     // ===================== X2 (next step's leading half): stB -> HBM, rho
     if (xv) {
-      const long long r0 = cell_row0(s);
+      double* dst = fout + (r0 + iv) * n_cols + cx * OX;
       for (int t = 0; t < lg; ++t) {
         const int r = t * OV + iv;
         double y[OX];
-        xapply(stB + r * rw + gl, y);
-        double* dst = fout + (r0 + r) * n_cols + cx * OX;
+        xapply(stB + r * rw, y);
+        const double wr = mcur[r];
 #pragma unroll
         for (int k = 0; k < OX; ++k) {
           dst[k] = y[k];
-          rha[k] = fma(mcur[r], y[k], rha[k]);
+          rha[k] = fma(wr, y[k], rha[k]);
         }
+        dst += (long long)OV * n_cols;
       }
     }
     g_cur = g_nxt;
@@ -348,8 +367,8 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   if (threads > 384) return no("fused step: rows wider than 384 columns");
   const int hl = (int)xp->halo_l, hr = (int)xp->halo_r;
   if (hl > xp->n_cells || hr > xp->n_cells) return no("fused step: shift wider than the row");
-  g.gl = ((hl * OX) + 1) & ~1;
-  g.rw = g.gl + (int)n_cols + (((hr * OX) + 1) & ~1);
+  g.gl = 0;
+  g.rw = (int)n_cols + (n_cols % 2 == 0 ? 1 : 0);   // odd row stride: conflict-free columns
   const size_t fixed = sizeof(double) * (size_t)xp->n_speeds * 2 * OX * OX + 5 * xp->n_speeds + 64 +
                        sizeof(double) * 6 * 8 * OV;
   const size_t budget = 227 * 1024 - 1024;
