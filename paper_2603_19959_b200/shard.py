@@ -230,6 +230,9 @@ class ShardedSimulation:
         self._rec = torch.empty(5, dtype=torch.float64, device=dev)
         self.t = 0.0
 
+    def fused_step_supported(self) -> bool:
+        return False   # the one-pass step needs whole rows; slabs use the separate passes
+
     # views ------------------------------------------------------------------
     def _local(self, buf):
         return buf[:, self.lw:self.lw + self.n_local * self.o]

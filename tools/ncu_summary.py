@@ -93,18 +93,21 @@ def main():
         open(os.path.join(ROOT, "profiles", f"{tag}_ncu_full.txt"), "w").write(
             "\n".join(lines) + "\n")
         print("\n".join(lines))
-        sweeps = [d for d in res if "k_sweep" in d["kernel"]]
-        if sweeps:
-            s = sweeps[0]
-            summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
-            summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
-            summ.setdefault(cfg, {})["sweep"] = {
+        summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
+        for key, pat in (("sweep", "k_sweep_stream"), ("step_fused", "k_step_fused"),
+                         ("xx", "k_xadv")):
+            hits = [d for d in res if pat in d["kernel"]]
+            if not hits:
+                continue
+            s = hits[-1]
+            summ.setdefault(cfg, {})[key] = {
                 "kernel": s["kernel"], "tag": tag,
                 "dram_bytes_per_launch": s["dram__bytes_read.sum"] + s["dram__bytes_write.sum"],
                 "duration_us_ncu": s["gpu__time_duration.sum"],
                 "dram_throughput_pct": s.get(
                     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")}
-            json.dump(summ, open(summ_path, "w"), indent=1)
+        json.dump(summ, open(summ_path, "w"), indent=1)
 
 
 if __name__ == "__main__":
