@@ -28,7 +28,7 @@ namespace sldg {
 constexpr int kStreamRing = 4;
 
 template <int O, int DIM>
-__global__ void __launch_bounds__(256, (O <= 3) ? 3 : 1)
+__global__ void __launch_bounds__(256, 1)
 k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
                long long ld, long long n_cols, const double* __restrict__ speeds, int bc,
                const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,

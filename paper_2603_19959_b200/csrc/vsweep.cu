@@ -348,25 +348,22 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
     return sizeof(double) * kStreamRing * R * cols * ctas <= budget;
   };
   if (al16 && n_cols % 2 == 0) {
-    // smallest line group that still leaves >= 9 rows of work per step, aiming for 4 CTAs/SM
-    for (int ctas : {4, 3, 2, 1}) {
-      for (int lines = 1; lines <= NL && tx_max == 0; ++lines) {
-        if (NL % lines || (!lines_contig && lines != NL)) continue;
-        if (DIM == 3 && lines * O < std::min(9, NLOC) && lines != NL) continue;
-        if (n_cols == ld && n_cols <= 256 && fits(lines, n_cols, ctas)) {
-          tx_max = (int)n_cols;
-          whole = 1;
-          lgl = lines;
-        } else {
-          for (int t = 256; t >= 64; t -= 32)
-            if (fits(lines, t, ctas)) {
-              tx_max = t;
-              lgl = lines;
-              break;
-            }
-        }
+    // whole cells per tile (measured fastest: one CTA per SM with all of a thread's
+    // lines in flight); smaller line groups only when a whole cell cannot fit
+    for (int lines = NL; lines >= 1 && tx_max == 0; --lines) {
+      if (NL % lines || (!lines_contig && lines != NL)) continue;
+      if (n_cols == ld && n_cols <= 256 && fits(lines, n_cols, 1)) {
+        tx_max = (int)n_cols;
+        whole = 1;
+        lgl = lines;
+      } else {
+        for (int t = 256; t >= 64; t -= 32)
+          if (fits(lines, t, 1)) {
+            tx_max = t;
+            lgl = lines;
+            break;
+          }
       }
-      if (tx_max) break;
     }
     if (!whole && tx_max > n_cols) tx_max = (int)((n_cols + 31) / 32 * 32);
   }
