@@ -377,11 +377,7 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
     SLDG_CUDA_TRY(cudaFuncSetAttribute(k_sweep_stream<O, DIM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int n_tiles = (int)((n_cols + tx_max - 1) / tx_max);
-    // persistent: one CTA per SM (the ring fills the shared memory), grid a multiple
-    // of the column-tile count; each CTA walks a strided item list
-    const long long items = p->n_walk * n_lg;
-    const long long per_tile = std::max<long long>(1, std::min<long long>(items, 148 / n_tiles));
-    const long long blocks = per_tile * n_tiles;
+    const long long blocks = p->n_walk * n_lg * n_tiles;
     k_sweep_stream<O, DIM><<<(unsigned)blocks, threads, smem, st>>>(
         p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, tx_max, n_tiles, whole,
         lgl, n_lg);
