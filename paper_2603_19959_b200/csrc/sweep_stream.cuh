@@ -25,7 +25,8 @@
 
 namespace sldg {
 
-constexpr int kStreamRing = 4;
+constexpr int kStreamRing = 5;     // cells s-1, s, s+1 in use + 2 in flight
+constexpr int kStreamAhead = kStreamRing - 3;
 
 template <int O, int DIM>
 __global__ void __launch_bounds__(256, 1)
@@ -140,13 +141,12 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     }
   };
   if (tid < 32) {
-    for (int k = 0; k < min(3, n_load); ++k) issue(k);
+    for (int k = 0; k < min(2 + kStreamAhead, n_load); ++k) issue(k);
   }
-  // per-line row offsets (compile-time for direction 0)
   for (int s = 0; s < n; ++s) {
-    // prefetch list position of virtual cell s+2
-    const int kn = s + 2 - v0;
-    if (tid < 32 && kn < n_load && kn >= 3) issue(kn);
+    // prefetch list position of virtual cell s+1+kStreamAhead
+    const int kn = s + 1 + kStreamAhead - v0;
+    if (tid < 32 && kn < n_load && kn >= 2 + kStreamAhead) issue(kn);
     // wait for virtual cells s-1 .. s+1 that exist in the list
     const int klo = max(s - 1 - v0, 0), khi = min(s + 1 - v0, n_load - 1);
     for (int k = klo; k <= khi; ++k) mbar_wait(&full[k % kStreamRing], (unsigned)((k / kStreamRing) & 1));
