@@ -25,30 +25,22 @@
 
 namespace sldg {
 
-constexpr int kStreamRing = 5;     // cells s-1, s, s+1 in use + 2 in flight
-constexpr int kStreamAhead = kStreamRing - 3;
+constexpr int kStreamRing = 4;
 
 template <int O, int DIM>
 __global__ void __launch_bounds__(256, 1)
 k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
                long long ld, long long n_cols, const double* __restrict__ speeds, int bc,
                const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
-               double* __restrict__ acc, int tx_max, int n_tiles, int whole_rows, int lgl,
-               int n_lg) {
+               double* __restrict__ acc, int tx_max, int n_tiles, int whole_rows) {
   constexpr int NL = (DIM == 3) ? O * O : 1;
   constexpr int NLOC = NL * O;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long full[kStreamRing];
   __shared__ int s_nsmin, s_nsmax;
 
-  // block -> (pencil, line group, column tile); a line group is lgl consecutive lines
-  // = lgl*O consecutive rows of every cell (direction 0), so a cell tile stays one block
-  const long long wq = blockIdx.x / n_tiles;
-  const int tile = (int)(blockIdx.x - wq * n_tiles);
-  const long long wp = wq / n_lg;
-  const int t0 = (int)(wq - wp * n_lg) * lgl;
-  const int roff = t0 * O;                      // first row of the group within a cell
-  const int R = (DIM == 3) ? lgl * O : NLOC;    // rows per tile
+  const long long wp = blockIdx.x / n_tiles;
+  const int tile = (int)(blockIdx.x - wp * n_tiles);
   const long long q = P.walk_pencils[wp];
   const long long off = P.p_off[q];
   const int n = P.p_n[q];
@@ -57,8 +49,8 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
   const int tid = threadIdx.x;
   const int lev = P.e_level[off];
   const int rstride = whole_rows ? (int)ld : tx_max;   // smem row stride (doubles)
-  const int cell_dbl = R * rstride;
-  const unsigned cell_bytes = (unsigned)(R * tx) * 8u;
+  const int cell_dbl = NLOC * rstride;
+  const unsigned cell_bytes = (unsigned)(NLOC * tx) * 8u;
 
   if (tid == 0) {
     s_nsmin = 1 << 30;
@@ -126,7 +118,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     const int v = v0 + k;
     const int cell = v < 0 ? n - 1 : (v >= n ? 0 : v);
     double* dst = sm + (k % kStreamRing) * cell_dbl;
-    const double* src = fin + (P.e_row0[off + cell] + roff) * ld + c0;
+    const double* src = fin + P.e_row0[off + cell] * ld + c0;
     unsigned long long* bar = &full[k % kStreamRing];
     if (whole_rows) {
       if (tid == 0) {
@@ -136,17 +128,18 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     } else {
       if (tid == 0) mbar_expect_tx(bar, cell_bytes);
       __syncwarp();
-      for (int r = tid; r < R; r += 32)
+      for (int r = tid; r < NLOC; r += 32)
         bulk_g2s(dst + r * rstride, src + (long long)r * ld, (unsigned)tx * 8u, bar);
     }
   };
   if (tid < 32) {
-    for (int k = 0; k < min(2 + kStreamAhead, n_load); ++k) issue(k);
+    for (int k = 0; k < min(3, n_load); ++k) issue(k);
   }
+  // per-line row offsets (compile-time for direction 0)
   for (int s = 0; s < n; ++s) {
-    // prefetch list position of virtual cell s+1+kStreamAhead
-    const int kn = s + 1 + kStreamAhead - v0;
-    if (tid < 32 && kn < n_load && kn >= 2 + kStreamAhead) issue(kn);
+    // prefetch list position of virtual cell s+2
+    const int kn = s + 2 - v0;
+    if (tid < 32 && kn < n_load && kn >= 3) issue(kn);
     // wait for virtual cells s-1 .. s+1 that exist in the list
     const int klo = max(s - 1 - v0, 0), khi = min(s + 1 - v0, n_load - 1);
     for (int k = klo; k <= khi; ++k) mbar_wait(&full[k % kStreamRing], (unsigned)((k / kStreamRing) & 1));
@@ -159,7 +152,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
       const double* me = sm + ((s - v0) % kStreamRing) * cell_dbl + tid;
       if (speed == 0.0) {
 #pragma unroll 3
-        for (int r = 0; r < R; ++r) dst[(r + roff) * dstride] = me[r * rstride];
+        for (int r = 0; r < NLOC; ++r) dst[r * dstride] = me[r * rstride];
       } else {
         // sources: virtual cells s - ns (same) and s - ns - 1 (neighbour)
         const int va_cell = s - (int)ns, vb_cell = s - (int)ns - 1;
@@ -169,11 +162,10 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
         const double* sb = sm + ((vb ? vb_cell : s) - v0) % kStreamRing * cell_dbl + tid;
 #pragma unroll
         for (int t = 0; t < NL; ++t) {
-          if (t < t0 || t >= t0 + ((DIM == 3) ? lgl : 1)) continue;
           double ua[O], ub[O], y[O];
 #pragma unroll
           for (int i = 0; i < O; ++i) {
-            const int r = ((DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i) - roff;
+            const int r = (DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i;
             ua[i] = va ? sa[r * rstride] : 0.0;
             ub[i] = vb ? sb[r * rstride] : 0.0;
           }

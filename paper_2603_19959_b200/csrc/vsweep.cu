@@ -334,53 +334,34 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
                         const long long* lm_ns, const double* lm_mats, double* acc,
                         cudaStream_t st) {
   constexpr int NLOC = Lines<O, DIM>::NLOC;
-  // streaming kernel geometry.  Line groups (direction 0: lgl consecutive lines are
-  // lgl*O consecutive rows of a cell) keep each cell tile one contiguous block while
-  // shrinking it so that several CTAs share an SM; whole rows per tile when they fit
-  // (one bulk copy per cell tile), else column tiles (one bulk copy per row).
+  // streaming kernel geometry: whole rows per cell when the tile spans the row
+  // (one bulk copy per cell), else column tiles with one bulk copy per row
   const size_t budget = 227 * 1024 - 256;
   const bool al16 = ((((unsigned long long)fin) & 15) == 0) && (ld % 2 == 0);
-  const int NL = Lines<O, DIM>::NL;
-  const bool lines_contig = DIM == 1 || p->direction == 0;
-  int tx_max = 0, whole = 0, lgl = NL;
-  auto fits = [&](int lines, long long cols, int ctas) {
-    const int R = DIM == 3 ? lines * O : NLOC;
-    return sizeof(double) * kStreamRing * R * cols * ctas <= budget;
-  };
-  if (al16 && n_cols % 2 == 0) {
-    // whole cells per tile (measured fastest: one CTA per SM with all of a thread's
-    // lines in flight); smaller line groups only when a whole cell cannot fit
-    for (int lines = NL; lines >= 1 && tx_max == 0; --lines) {
-      if (NL % lines || (!lines_contig && lines != NL)) continue;
-      if (n_cols == ld && n_cols <= 256 && fits(lines, n_cols, 1)) {
-        tx_max = (int)n_cols;
-        whole = 1;
-        lgl = lines;
-      } else {
-        for (int t = 256; t >= 64; t -= 32)
-          if (fits(lines, t, 1)) {
-            tx_max = t;
-            lgl = lines;
-            break;
-          }
+  int tx_max = 0, whole = 0;
+  if (al16 && n_cols == ld && n_cols <= 256 && (NLOC * n_cols) % 2 == 0 &&
+      sizeof(double) * kStreamRing * NLOC * n_cols <= budget) {
+    tx_max = (int)n_cols;
+    whole = 1;
+  } else if (al16 && n_cols % 2 == 0) {
+    for (int t = 256; t >= 32; t -= 32)
+      if (sizeof(double) * kStreamRing * NLOC * t <= budget) {
+        tx_max = t;
+        break;
       }
-    }
-    if (!whole && tx_max > n_cols) tx_max = (int)((n_cols + 31) / 32 * 32);
+    if (tx_max > n_cols) tx_max = (int)((n_cols + 31) / 32 * 32);
   }
-  if (DIM == 1) lgl = 1;
-  const int n_lg = NL / lgl;
   const bool use_stream = !force_slow && p->n_walk > 0 && tx_max > 0 && n_cols >= 2;
   if (use_stream) {
     const int threads = (tx_max + 31) / 32 * 32;
     const int rstride = whole ? (int)ld : tx_max;
-    const size_t smem = sizeof(double) * (size_t)kStreamRing * (DIM == 3 ? lgl * O : NLOC) * rstride;
+    const size_t smem = sizeof(double) * (size_t)kStreamRing * NLOC * rstride;
     SLDG_CUDA_TRY(cudaFuncSetAttribute(k_sweep_stream<O, DIM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int n_tiles = (int)((n_cols + tx_max - 1) / tx_max);
-    const long long blocks = p->n_walk * n_lg * n_tiles;
+    const long long blocks = p->n_walk * n_tiles;
     k_sweep_stream<O, DIM><<<(unsigned)blocks, threads, smem, st>>>(
-        p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, tx_max, n_tiles, whole,
-        lgl, n_lg);
+        p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, tx_max, n_tiles, whole);
     SLDG_LAUNCH_CHECK("k_sweep_stream");
     if (p->n_gen > 0) {
       long long n = p->n_gen * n_cols;
