@@ -119,6 +119,11 @@ typedef struct SldgXPlanDesc {
 
 int sldg_xplan_create(const SldgXPlanDesc* desc, sldg_xplan** out);
 int sldg_xplan_destroy(sldg_xplan* plan);
+/* Declare the velocity layout of the rows: n_rows = cells x o_v^3 and every row
+ * b = i + o_v j + o_v^2 k of a cell has the speed of its v_x node i (true for the
+ * driver's v_x speeds).  Verified on the host; enables the same-speed row-tile x
+ * kernel (csrc/xx_tiles.cuh). */
+int sldg_xplan_set_vlayout(sldg_xplan* plan, int32_t o_v);
 /* max |n_shift| and max n_shift+1 over rows: halo cells needed [left, right] */
 int sldg_xplan_halo(const sldg_xplan* plan, int64_t* left_right);
 

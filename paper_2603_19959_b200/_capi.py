@@ -91,6 +91,7 @@ _SIGS = {
     "sldg_xplan_create": (C.c_int, [C.POINTER(SldgXPlanDesc), C.POINTER(C.c_void_p)]),
     "sldg_xplan_destroy": (C.c_int, [C.c_void_p]),
     "sldg_xplan_halo": (C.c_int, [C.c_void_p, c_int64_p]),
+    "sldg_xplan_set_vlayout": (C.c_int, [C.c_void_p, C.c_int32]),
     "sldg_advect_x": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     "sldg_xadv_scratch_bytes": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t)]),
     "sldg_advect_x_fused": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,

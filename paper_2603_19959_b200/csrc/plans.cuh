@@ -60,6 +60,8 @@ struct sldg_xplan {
   int o;
   long long n_cells, n_rows, n_speeds;
   long long halo_l, halo_r;
+  int vo;          // velocity nodes per direction when rows are cells x o^3 with a
+                   // per-(cell, v_x node) speed (sldg_xplan_set_vlayout); 0 = unknown
   double h, dt;
   void* block;
 };

@@ -434,6 +434,79 @@ static int launch_xadv(const sldg_xplan* X, const double* fin, long long ld_in, 
   return SLDG_ERR_ARG;
 }
 
+}  // namespace sldg
+
+#include "xx_tiles.cuh"
+
+namespace sldg {
+
+// Geometry of k_xx_tiles: depends only on the problem shape (bitwise-stable sums).
+static XTGeom xt_geom(const sldg_xplan* X) {
+  XTGeom g{};
+  g.ok = false;
+  const int ov = X->vo, ox = X->o;
+  const long long nxc = X->n_cells;
+  if (ov < 2 || ov > 4 || ox < 2 || ox > 4 || nxc > 512 || X->n_rows == 0) return g;
+  const int nl = ov * ov, nloc = nl * ov;
+  if (X->n_rows % nloc != 0) return g;
+  g.tpc = (int)std::max<long long>(1, std::min<long long>(kXTMaxTpc, 512 / nxc));
+  g.threads = (int)((g.tpc * nxc + 31) / 32 * 32);
+  if (g.threads < 64) g.threads = 64;
+  const long long row_len = nxc * ox;
+  const size_t table = sizeof(double) * X->n_speeds * 2 * ox * ox + 5 * X->n_speeds + 64;
+  const size_t budget = 227 * 1024 - 1024;
+  for (int nring : {3, 2}) {
+    for (int rpt = nl; rpt >= 1 && !g.ok; --rpt) {
+      if (nl % rpt) continue;
+      const size_t slot = (size_t)g.tpc * rpt * row_len;
+      const size_t smem = sizeof(double) * ((nring + 1) * slot + (size_t)nring * g.tpc * rpt * 3) + table;
+      if (smem <= budget && sizeof(double) * nring * slot >= sizeof(double) * 3 * g.threads) {
+        g.rpt = rpt;
+        g.nring = nring;
+        g.smem = smem;
+        g.ok = true;
+      }
+    }
+    if (g.ok) break;
+  }
+  if (!g.ok) return g;
+  g.n_tiles = (X->n_rows / nloc) * (nl / g.rpt) * ov;
+  g.n_groups = (g.n_tiles + g.tpc - 1) / g.tpc;
+  const long long ctas_sm = std::max<long long>(1, std::min<long long>(
+      (long long)(227 * 1024 / g.smem), 2048 / g.threads));
+  g.n_groups = std::max<long long>(1, g.n_groups);
+  g.grid_ = std::min<long long>(g.n_groups, 148LL * ctas_sm);
+  return g;
+}
+
+template <int OV, int OX>
+static int launch_xt_t(const sldg_xplan* X, const XTGeom& g, const double* fin, double* fout,
+                       long long ld, int napply, bool mom, bool rho, const XEpi& epi,
+                       cudaStream_t st) {
+  auto k = k_xx_tiles<OV, OX>;
+  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  k<<<(unsigned)g.grid_, g.threads, g.smem, st>>>(X->dev, fin, fout, ld, X->n_rows,
+                                                  (int)X->n_cells, g.rpt, g.tpc, g.nring,
+                                                  (int)X->n_speeds, epi, napply, mom ? 1 : 0,
+                                                  rho ? 1 : 0);
+  SLDG_LAUNCH_CHECK("k_xx_tiles");
+  return SLDG_OK;
+}
+
+static int launch_xt(const sldg_xplan* X, const XTGeom& g, const double* fin, double* fout,
+                     long long ld, int napply, bool mom, bool rho, const XEpi& epi,
+                     cudaStream_t st) {
+  switch (X->vo * 10 + X->o) {
+#define CASE(A, B) \
+  case A * 10 + B: return launch_xt_t<A, B>(X, g, fin, fout, ld, napply, mom, rho, epi, st);
+    CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(4, 2) CASE(4, 3)
+    CASE(4, 4)
+#undef CASE
+  }
+  set_error("x tile kernel: unsupported degrees");
+  return SLDG_ERR_UNSUPPORTED;
+}
+
 // 16-byte-aligned rows: the specialised kernel is allowed (its geometry then fixes the
 // row partition of every pass on these buffers)
 static bool xadv_vec(const sldg_xplan* X, const double* fin, const double* fout, long long ld_in,
@@ -575,6 +648,32 @@ int sldg_xplan_halo(const sldg_xplan* X, int64_t* lr) {
   return SLDG_OK;
 }
 
+int sldg_xplan_set_vlayout(sldg_xplan* X, int32_t o_v) {
+  if (!X || o_v < 1) {
+    set_error("bad argument");
+    return SLDG_ERR_ARG;
+  }
+  const long long nloc = (long long)o_v * o_v * o_v;
+  if (X->n_rows % nloc != 0) {
+    set_error("rows are not cells x o_v^3");
+    return SLDG_ERR_ARG;
+  }
+  std::vector<int> rs(X->n_rows);
+  cudaError_t ce = cudaMemcpy(rs.data(), X->dev.row_speed, sizeof(int) * X->n_rows,
+                              cudaMemcpyDeviceToHost);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemcpy(row_speed)");
+  // every row b = i + o j + o^2 k of a cell must share the speed of its v_x node i
+  for (long long r = 0; r < X->n_rows; ++r) {
+    const long long cell = r / nloc, b = r - cell * nloc;
+    if (rs[r] != rs[cell * nloc + b % o_v]) {
+      set_error("row speeds are not constant per (cell, v_x node)");
+      return SLDG_ERR_ARG;
+    }
+  }
+  X->vo = o_v;
+  return SLDG_OK;
+}
+
 int sldg_advect_x(const sldg_xplan* X, const double* fin, double* fout, int64_t ld, void* stream) {
   if (!X || !fin || !fout || fin == fout || ld < X->n_cells * X->o) {
     set_error("bad advect_x arguments (f_in and f_out must be distinct device buffers)");
@@ -583,6 +682,10 @@ int sldg_advect_x(const sldg_xplan* X, const double* fin, double* fout, int64_t 
   if (X->n_rows == 0) return SLDG_OK;
   cudaStream_t st = (cudaStream_t)stream;
   XEpi epi{};
+  {
+    XTGeom tg = xt_geom(X);
+    if (tg.ok) return launch_xt(X, tg, fin, fout, ld, 1, false, false, epi, st);
+  }
   switch (X->o) {
 #define CASE(O)                                                                     \
   case O:                                                                           \
@@ -607,7 +710,10 @@ int sldg_xadv_scratch_bytes(const sldg_xplan* X, size_t* bytes) {
     return SLDG_ERR_ARG;
   }
   XadvGeom g = xadv_geom(X, 2, true, true), g2 = xadv_geom(X, 2, true, false);
-  *bytes = sizeof(double) * (size_t)std::max(g.grid, g2.grid) * (3 + X->n_cells * X->o) + 256;
+  XTGeom tg = xt_geom(X);
+  long long grid = std::max(g.grid, g2.grid);
+  if (tg.ok) grid = std::max(grid, tg.grid_);
+  *bytes = sizeof(double) * (size_t)grid * (3 + X->n_cells * X->o) + 256;
   return SLDG_OK;
 }
 
@@ -625,23 +731,29 @@ int sldg_advect_x_fused(const sldg_xplan* X, const double* fin, double* fout, in
   if (X->n_rows == 0) return SLDG_OK;
   cudaStream_t st = (cudaStream_t)stream;
   XadvGeom g = xadv_geom(X, n_apply, rho, xadv_vec(X, fin, fout, ld, ld));
+  const XTGeom tg = xt_geom(X);
+  if (tg.ok) g.grid = (int)tg.grid_;   // partials are per CTA of the kernel that runs
   XEpi epi{w, v0, v2, xw, nullptr, nullptr};
   if (scratch) {
     epi.mom_part = (double*)scratch;
     epi.rho_part = (double*)scratch + 3 * (size_t)g.grid;
   }
   int rc = SLDG_ERR_UNSUPPORTED;
-  if (!g.ok) {
-    set_error("fused x pass: row too long for the shared-memory ring");
-    return rc;
-  }
-  switch (X->o) {
+  if (tg.ok) {
+    rc = launch_xt(X, tg, fin, fout, ld, n_apply, mom, rho, epi, st);
+  } else {
+    if (!g.ok) {
+      set_error("fused x pass: row too long for the shared-memory ring");
+      return rc;
+    }
+    switch (X->o) {
 #define CASE(O) \
   case O: rc = launch_xadv<O>(X, fin, ld, fout, ld, n_apply, mom, rho, epi, g, st); break;
-    CASE(2) CASE(3) CASE(4)
+      CASE(2) CASE(3) CASE(4)
 #undef CASE
-    default:
-      set_error("fused x pass compiled for degree_x <= 3");
+      default:
+        set_error("fused x pass compiled for degree_x <= 3");
+    }
   }
   if (rc) return rc;
   if (mom) {

@@ -1,0 +1,255 @@
+// xx_tiles.cuh -- x-advection over "same-speed" row tiles (included by xfield.cu).
+//
+// xfield.advect_x (xfield.py:82-104) applies, per velocity row, the periodic
+// two-cell update out_c = A u_{c-n} + B u_{c-n-1} (sldg1d.py:124-136) with the
+// (n, A, B) of the row's v_x.  Rows b = i + o j + o^2 k of one velocity cell
+// with the same v_x node i share v_x, hence one (n, A, B).  A tile is RPT such
+// rows of one cell (rows cell*o^3 + (t0 + u)*o + i, u < RPT); a CTA processes
+// TPC tiles at a time, thread = (tile, x cell), so the matrices are loaded into
+// registers once per tile and every source read is conflict-free (consecutive
+// threads read consecutive cells).  Rows arrive by 1-D TMA bulk copies into a
+// ring of tile groups (mbarrier per slot), one group ahead of the compute.
+//   NAPPLY == 2 : out = X(X(in)) (trailing half step of step n + leading half
+//                 step of step n+1), the intermediate row in shared memory
+//   MOM         : (m0, m1, m2) of the state after the FIRST application
+//   RHO         : rho = w . f of the final output
+// Per-thread column accumulators; CTA partials in a fixed order; the grid
+// depends only on the problem shape (bitwise-reproducible reductions).
+// Arithmetic per output identical to k_xadv / k_advect_x.
+#pragma once
+
+#include "tma_util.cuh"
+
+namespace sldg {
+
+struct XTGeom {
+  int rpt, tpc, nring, threads;   // rows per tile, tiles per CTA step, ring depth, threads
+  long long n_tiles, n_groups, grid_;
+  size_t smem;
+  bool ok;
+};
+
+constexpr int kXTMaxTpc = 8;
+
+template <int OV, int OX>
+__global__ void __launch_bounds__(512, 1)
+k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout, long long ld,
+           long long n_rows, int n_xc, int rpt, int tpc, int nring, int n_speeds, XEpi epi,
+           int napply, int mom, int rho) {
+  constexpr int NL = OV * OV, NLOC = NL * OV;
+  constexpr int XM = 2 * OX * OX;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) unsigned long long full[4];
+  const int row_len = n_xc * OX;
+  const int tid = threadIdx.x;
+  const int tt = tid / n_xc;                 // tile within the group
+  const int cx = tid - tt * n_xc;            // x cell
+  const bool act = tt < tpc;
+  const int per_cell = (NL / rpt) * OV;      // tiles per velocity cell
+  const long long n_tiles = (n_rows / NLOC) * per_cell;
+  const long long n_groups = (n_tiles + tpc - 1) / tpc;
+  const int slot_dbl = tpc * rpt * row_len;
+  double* ring = sm;
+  double* mid = ring + (long long)nring * slot_dbl;
+  double* meta = mid + slot_dbl;             // [nring][tpc][rpt][3]: w, w*v0, w*v2
+  double* xtab = meta + (long long)nring * tpc * rpt * 3;   // per speed: A | B
+  int* xnsm = reinterpret_cast<int*>(xtab + (long long)n_speeds * XM);
+  unsigned char* xid = reinterpret_cast<unsigned char*>(xnsm + n_speeds);
+  for (int k = tid; k < n_speeds * XM; k += blockDim.x) xtab[k] = __ldg(X.mats + k);
+  for (int k = tid; k < n_speeds; k += blockDim.x) {
+    xnsm[k] = __ldg(X.nsm + k);
+    xid[k] = X.ident[k];
+  }
+
+  // tile id -> first row and row stride (rows u = 0..rpt-1 are row0 + u*OV)
+  auto tile_row0 = [&](long long tile) -> long long {
+    const long long cell = tile / per_cell;
+    const int rem = (int)(tile - cell * per_cell);
+    const int iv = rem % OV, tg = rem / OV;
+    return cell * NLOC + (long long)tg * rpt * OV + iv;
+  };
+
+  if (tid == 0) {
+    for (int k = 0; k < nring; ++k) mbar_init(&full[k], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const long long g0 = blockIdx.x, gs = gridDim.x;
+  const long long my = g0 < n_groups ? (n_groups - g0 + gs - 1) / gs : 0;
+  // issue group i (of this CTA) into slot i % nring: one bulk copy per row (warp 0),
+  // metadata by plain loads (threads of warp 1) into the slot's meta block
+  auto issue = [&](long long i) {
+    const int s = (int)(i % nring);
+    const long long grp = g0 + i * gs;
+    const long long t_first = grp * tpc;
+    const int nt = (int)min((long long)tpc, n_tiles - t_first);
+    if (tid < 32) {
+      if (tid == 0) mbar_expect_tx(&full[s], (unsigned)(nt * rpt * row_len * 8));
+      __syncwarp();
+      for (int q = tid; q < nt * rpt; q += 32) {
+        const int ti = q / rpt, u = q - ti * rpt;
+        const long long row = tile_row0(t_first + ti) + (long long)u * OV;
+        bulk_g2s(ring + (long long)s * slot_dbl + (ti * rpt + u) * row_len, fin + row * ld,
+                 (unsigned)(row_len * 8), &full[s]);
+      }
+    } else if (tid < 64 && (mom || rho)) {
+      for (int q = tid - 32; q < nt * rpt; q += 32) {
+        const int ti = q / rpt, u = q - ti * rpt;
+        const long long row = tile_row0(t_first + ti) + (long long)u * OV;
+        const double w = __ldg(epi.w + row);
+        double* m = meta + (((long long)s * tpc + ti) * rpt + u) * 3;
+        m[0] = w;
+        if (mom) {
+          m[1] = w * __ldg(epi.v0 + row);
+          m[2] = w * __ldg(epi.v2 + row);
+        }
+      }
+    }
+  };
+  for (long long i = 0; i < min((long long)nring - 1, my); ++i) issue(i);
+
+  double m0a[OX], m1a[OX], m2a[OX], rha[OX];
+#pragma unroll
+  for (int k = 0; k < OX; ++k) m0a[k] = m1a[k] = m2a[k] = rha[k] = 0.0;
+
+  auto speed_of = [&](long long i) -> int {   // this thread's tile speed in group i
+    const long long tile = (g0 + i * gs) * tpc + tt;
+    return (act && i < my && tile < n_tiles) ? __ldg(X.row_speed + tile_row0(tile)) : 0;
+  };
+  int g_next = speed_of(0);
+  for (long long i = 0; i < my; ++i) {
+    if (i + nring - 1 < my) issue(i + nring - 1);
+    const int g = g_next;
+    g_next = speed_of(i + 1);                 // prefetched one group ahead
+    const int s = (int)(i % nring);
+    mbar_wait(&full[s], (unsigned)((i / nring) & 1));
+    __syncthreads();                          // metadata of slot s visible
+    const long long t_first = (g0 + i * gs) * tpc;
+    const long long tile = t_first + tt;
+    const bool live = act && tile < n_tiles;
+    double xa[OX * OX], xb[OX * OX];
+    bool ident = true;
+    int ia = 0, ib = 0;
+    long long row0 = 0;
+    if (live) {
+      row0 = tile_row0(tile);
+      ident = xid[g] != 0;
+      const double* AB = xtab + (long long)g * XM;
+#pragma unroll
+      for (int k = 0; k < OX * OX; ++k) {
+        xa[k] = AB[k];
+        xb[k] = AB[OX * OX + k];
+      }
+      int a = cx - xnsm[g];   // nsm in [0, n_xc): the periodic source cell of cx
+      if (a < 0) a += n_xc;
+      ia = (ident ? cx : a) * OX;
+      ib = (a == 0 ? n_xc - 1 : a - 1) * OX;
+    }
+    auto xapply = [&](const double* srow, double* y) {
+      if (ident) {
+#pragma unroll
+        for (int k = 0; k < OX; ++k) y[k] = srow[ia + k];
+        return;
+      }
+      double ua[OX], ub[OX];
+#pragma unroll
+      for (int j = 0; j < OX; ++j) {
+        ua[j] = srow[ia + j];
+        ub[j] = srow[ib + j];
+      }
+#pragma unroll
+      for (int k = 0; k < OX; ++k) {
+        double sa = xa[k * OX] * ua[0];
+        double sb = xb[k * OX] * ub[0];
+#pragma unroll
+        for (int j = 1; j < OX; ++j) {
+          sa = fma(xa[k * OX + j], ua[j], sa);
+          sb = fma(xb[k * OX + j], ub[j], sb);
+        }
+        y[k] = sa + sb;
+      }
+    };
+    const double* src = ring + (long long)s * slot_dbl + tt * rpt * row_len;
+    const double* mt = meta + ((long long)s * tpc + tt) * rpt * 3;
+    double* md = mid + tt * rpt * row_len;
+    if (napply == 2) {
+      if (live) {
+        for (int u = 0; u < rpt; ++u) {
+          double y[OX];
+          xapply(src + u * row_len, y);
+#pragma unroll
+          for (int k = 0; k < OX; ++k) md[u * row_len + cx * OX + k] = y[k];
+          if (mom) {
+#pragma unroll
+            for (int k = 0; k < OX; ++k) {
+              m0a[k] = fma(mt[u * 3], y[k], m0a[k]);
+              m1a[k] = fma(mt[u * 3 + 1], y[k], m1a[k]);
+              m2a[k] = fma(mt[u * 3 + 2], y[k], m2a[k]);
+            }
+          }
+        }
+      }
+      __syncthreads();
+      src = md;
+    }
+    if (live) {
+      for (int u = 0; u < rpt; ++u) {
+        double y[OX];
+        xapply(src + u * row_len, y);
+        double* dst = fout + (row0 + (long long)u * OV) * ld + cx * OX;
+#pragma unroll
+        for (int k = 0; k < OX; ++k) {
+          dst[k] = y[k];
+          if (rho) rha[k] = fma(mt[u * 3], y[k], rha[k]);
+          if (mom && napply == 1) {
+            m0a[k] = fma(mt[u * 3], y[k], m0a[k]);
+            m1a[k] = fma(mt[u * 3 + 1], y[k], m1a[k]);
+            m2a[k] = fma(mt[u * 3 + 2], y[k], m2a[k]);
+          }
+        }
+      }
+    }
+    __syncthreads();                          // slot s and mid are reused next
+  }
+
+  // CTA partials: rho per column (tiles of the group summed in order), moments
+  // contracted with the x weights and summed over threads in order
+  double* red = sm;
+  if (rho) {
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < OX; ++k) red[tt * row_len + cx * OX + k] = rha[k];
+    }
+    __syncthreads();
+    for (int e = tid; e < row_len; e += blockDim.x) {
+      double v = 0.0;
+      for (int q = 0; q < tpc; ++q) v += red[q * row_len + e];
+      epi.rho_part[(long long)blockIdx.x * row_len + e] = v;
+    }
+    __syncthreads();
+  }
+  if (mom) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < OX; ++k) {
+        const double xwk = __ldg(epi.xw + cx * OX + k);
+        s0 = fma(xwk, m0a[k], s0);
+        s1 = fma(xwk, m1a[k], s1);
+        s2 = fma(xwk, m2a[k], s2);
+      }
+    }
+    red[tid] = s0;
+    red[blockDim.x + tid] = s1;
+    red[2 * blockDim.x + tid] = s2;
+    __syncthreads();
+    if (tid < 3) {
+      double v = 0.0;
+      for (int q = 0; q < (int)blockDim.x; ++q) v += red[tid * blockDim.x + q];
+      epi.mom_part[blockIdx.x * 3 + tid] = v;
+    }
+  }
+}
+
+}  // namespace sldg

@@ -79,6 +79,10 @@ class XAdvectionPlan:
             out = C.c_void_p()
             _capi.check(_capi.lib().sldg_xplan_create(C.byref(desc), C.byref(out)), ValueError)
             h = out.value
+            if getattr(self, "velocity_order", None):
+                # rows are velocity cells x o^3 with one speed per (cell, v_x node):
+                # enables the same-speed row-tile kernel (verified by the library)
+                _capi.lib().sldg_xplan_set_vlayout(h, int(self.velocity_order))
             self._dev[key] = h
         return h
 
