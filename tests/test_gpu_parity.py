@@ -416,3 +416,27 @@ def test_run_uses_fused_step_and_matches_step_loop():
     for x, y in zip(res.records, recs):
         assert abs(x.m0 - y.m0) <= 1e-13 * abs(y.m0)
         assert abs(x.e_max - y.e_max) <= 1e-10 * abs(recs[0].e_max)
+
+
+@pytest.mark.parametrize("direction", [1, 2])
+@pytest.mark.parametrize("nb,lv,p,bc", [(4, 1, 2, "absorbing"), (4, 1, 3, "periodic"),
+                                        (6, 0, 2, "absorbing"), (5, 2, 1, "periodic")])
+def test_sweep_other_directions_vs_oracle(direction, nb, lv, p, bc):
+    """v_y / v_z sweeps: plans for directions 1 and 2 use the same kernels."""
+    rng = np.random.default_rng(direction * 100 + nb + lv + p)
+    m = sv.build_mesh(3, nb, lv, 6.0)
+    b = sv.DGBasis(p)
+    ps = sv.classify_conforming(sv.extract_pencils(m, direction), m, bc)
+    plan = sv.build_sweep_plan(m, ps, sv.build_permutation(b, 3), b)
+    om = so.make_mesh(3, nb, lv, 6.0)
+    oplan = so.make_plan(om, so.mark_conforming(so.make_pencils(om, direction), bc), p)
+    f = rng.standard_normal((plan.n_dofs, 34))
+    speeds = rng.uniform(-1.5, 1.5, 34) * 0.2
+    speeds[2] = 0.0
+    speeds[4] *= 30.0
+    ref = so.advect_v(f.copy(), speeds, 0.1, oplan, bc)
+    fd = dev(f)
+    sv.advect_velocity(fd, speeds, 0.1, plan, bc=bc)
+    got = fd.cpu().numpy()
+    assert np.abs(got - ref).max() <= TOL * np.abs(ref).max()
+    assert np.array_equal(got[:, 2], f[:, 2])
