@@ -85,9 +85,9 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   double* stA = ring + kFRing * tile;
   double* stB = stA + R * rw;
   double* xtab = stB + R * rw;                  // n_speeds x (A|B) for the x shift
-  double* meta = xtab + (long long)n_speeds * XM;   // [2][3][R]: w, w*v0, w*v2 per tile row
-  int* xns = reinterpret_cast<int*>(meta + 6 * R);
+  int* xns = reinterpret_cast<int*>(xtab + (long long)n_speeds * XM);
   unsigned char* xid = reinterpret_cast<unsigned char*>(xns + n_speeds);
+  double* meta = xtab + (long long)n_speeds * XM + (n_speeds * 5 + 15) / 8 + 1;   // per-pencil tables
 
   const long long wp = blockIdx.x / n_lg;
   const int t0 = (int)(blockIdx.x - wp * n_lg) * lg;   // first line of the group
@@ -138,24 +138,26 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
 #pragma unroll
   for (int k = 0; k < OX; ++k) m0a[k] = m1a[k] = m2a[k] = rha[k] = 0.0;
 
-  // per-cell x metadata, prefetched one cell ahead: thread q < 3R loads one of
-  // (w, w*v0, w*v2) of one tile row into a register, parks it in the meta buffer
-  auto cell_row0 = [&](int s) { return P.e_row0[off + s] + (long long)t0 * OV; };
-  auto fetch_meta = [&](int s) -> double {
-    if (tid >= 3 * R || s >= n) return 0.0;
-    const int kind = tid / R, r = tid - kind * R;
-    const long long row = cell_row0(s) + r;
+  // per-pencil metadata, loaded once into shared memory (no global loads in the
+  // step loop): tile row base per cell, x-speed index per (cell, v_x node) and
+  // (w, w*v0, w*v2) per tile row of every cell
+  long long* crow = reinterpret_cast<long long*>(meta);                   // [n]
+  int* cg = reinterpret_cast<int*>(crow + n);                               // [n][OV]
+  double* cmeta = reinterpret_cast<double*>(cg + ((n * OV + 1) & ~1));      // [n][3][R]
+  for (int k = tid; k < n; k += blockDim.x) crow[k] = P.e_row0[off + k] + (long long)t0 * OV;
+  __syncthreads();
+  for (int k = tid; k < n * OV; k += blockDim.x)
+    cg[k] = __ldg(X.row_speed + crow[k / OV] + k % OV);
+  for (int k = tid; k < n * R; k += blockDim.x) {
+    const int s2 = k / R, r = k - s2 * R;
+    const long long row = crow[s2] + r;
     const double wr = __ldg(fa.w + row);
-    return kind == 0 ? wr : wr * __ldg((kind == 1 ? fa.v0 : fa.v2) + row);
-  };
-  auto fetch_g = [&](int s) -> int {
-    return (xv && s < n) ? __ldg(X.row_speed + cell_row0(s) + iv) : 0;
-  };
-  {
-    const double m = fetch_meta(0);
-    if (tid < 3 * R) meta[tid] = m;
+    double* m = cmeta + (long long)s2 * 3 * R;
+    m[r] = wr;
+    m[R + r] = wr * __ldg(fa.v0 + row);
+    m[2 * R + r] = wr * __ldg(fa.v2 + row);
   }
-  int g_cur = fetch_g(0);
+  auto cell_row0 = [&](int s) -> long long { return crow[s]; };
   __syncthreads();
 
   // ---- ring of cell tiles (as k_sweep_stream)
@@ -172,21 +174,21 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     for (int k = 0; k < min(3, n_load); ++k) issue(k);
 
   for (int s = 0; s < n; ++s) {
-    const double meta_nxt = fetch_meta(s + 1);
-    const int g_nxt = fetch_g(s + 1);
-    const double* mcur = meta + (s & 1) * 3 * R;
+    const double* mcur = cmeta + (long long)s * 3 * R;
     const long long r0 = cell_row0(s);
+    const int g_cur = xv ? cg[s * OV + iv] : 0;
     // ===================== V: pencil sweep of cell s -> stA (rows of R, stride rw)
     if (streamable) {
       const int kn = s + 2 - v0c;
       if (tid == 0 && kn < n_load && kn >= 3) issue(kn);
       const int klo = max(s - 1 - v0c, 0), khi = min(s + 1 - v0c, n_load - 1);
-      for (int k = klo; k <= khi; ++k) mbar_wait(&full[k % kFRing], (unsigned)((k / kFRing) & 1));
+      for (int k = klo; k <= khi; ++k)
+        mbar_wait(&full[k & (kFRing - 1)], (unsigned)(((unsigned)k / kFRing) & 1));
     }
     if (colv) {
       double* out = stA + c;
       if (speed == 0.0) {
-        const double* me = streamable ? ring + ((s - v0c) % kFRing) * tile + c
+        const double* me = streamable ? ring + ((s - v0c) & (kFRing - 1)) * tile + c
                                       : fin + r0 * n_cols + c;
         for (int r = 0; r < R; ++r) out[r * rw] = me[r * n_cols];
       } else {
@@ -196,8 +198,8 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
         if (streamable) {
           va = per || (va_cell >= 0 && va_cell < n);
           vb = per || (vb_cell >= 0 && vb_cell < n);
-          sa = ring + ((va ? va_cell : s) - v0c) % kFRing * tile + c;
-          sb = ring + ((vb ? vb_cell : s) - v0c) % kFRing * tile + c;
+          sa = ring + (((va ? va_cell : s) - v0c) & (kFRing - 1)) * tile + c;
+          sb = ring + (((vb ? vb_cell : s) - v0c) & (kFRing - 1)) * tile + c;
         } else {
           long long qa = va_cell, qb = vb_cell;
           if (per) {
@@ -303,8 +305,6 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
         dst += (long long)OV * n_cols;
       }
     }
-    g_cur = g_nxt;
-    if (tid < 3 * R) meta[((s + 1) & 1) * 3 * R + tid] = meta_nxt;
     __syncthreads();   // ring slot of cell s-1, stA/stB and the meta buffer are reused next
   }
 
@@ -369,14 +369,16 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   if (hl > xp->n_cells || hr > xp->n_cells) return no("fused step: shift wider than the row");
   g.gl = 0;
   g.rw = (int)n_cols + (n_cols % 2 == 0 ? 1 : 0);   // odd row stride: conflict-free columns
-  const size_t fixed = sizeof(double) * (size_t)xp->n_speeds * 2 * OX * OX + 5 * xp->n_speeds + 64 +
-                       sizeof(double) * 6 * 8 * OV;
+  const size_t fixed = sizeof(double) * (size_t)xp->n_speeds * 2 * OX * OX +
+                       sizeof(double) * ((xp->n_speeds * 5 + 15) / 8 + 1) + 64;
+  const size_t nmax = (size_t)vp->max_pencil_cells;
   const size_t budget = 227 * 1024 - 1024;
   g.lg = 0;
   for (int lg = std::min(8, OV * OV); lg >= 1; --lg) {
     if ((OV * OV) % lg) continue;
     const size_t R = (size_t)lg * OV;
-    const size_t smem = sizeof(double) * (kFRing * R * n_cols + 2 * R * g.rw) + fixed;
+    const size_t tables = 8 * nmax + 4 * ((nmax * OV + 1) & ~(size_t)1) + 8 * nmax * 3 * R;
+    const size_t smem = sizeof(double) * (kFRing * R * n_cols + 2 * R * g.rw) + fixed + tables;
     const size_t red = sizeof(double) * std::max<size_t>(OV * n_cols, 3 * threads);
     if (smem <= budget && sizeof(double) * 2 * R * g.rw >= red) {
       // prefer two CTAs per SM when possible
