@@ -28,6 +28,7 @@
 // host falls back to the separate passes.
 #include <algorithm>
 #include <string>
+#include <type_traits>
 
 #include "plans.cuh"
 #include "sldg_common.cuh"
@@ -68,40 +69,45 @@ struct FusedArgs {
   double* rho_part;   // [grid][n_cols]
 };
 
-template <int OV, int OX>
+template <bool B>
+using BoolC = std::integral_constant<bool, B>;
+
+template <int OV, int OX, int LG>
 __global__ void __launch_bounds__(384, 1)
 k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout,
              int n_cols, int n_xc, const double* __restrict__ speeds, int bc,
-             const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats, int lg,
-             int n_lg, int hl, int hr, int gl, int rw, int n_speeds, FusedArgs fa) {
+             const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats, int rw,
+             int n_speeds, FusedArgs fa) {
   constexpr int XM = 2 * OX * OX;
+  constexpr int R = LG * OV;                    // rows per tile
+  constexpr int n_lg = OV * OV / LG;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long full[kFRing];
   __shared__ int s_nsmin, s_nsmax;
 
-  const int R = lg * OV;                        // rows per tile
   const int tile = R * n_cols;                  // doubles per ring slot
   double* ring = sm;
   double* stA = ring + kFRing * tile;
   double* stB = stA + R * rw;
   double* xtab = stB + R * rw;                  // n_speeds x (A|B) for the x shift
   int* xns = reinterpret_cast<int*>(xtab + (long long)n_speeds * XM);
-  unsigned char* xid = reinterpret_cast<unsigned char*>(xns + n_speeds);
-  double* meta = xtab + (long long)n_speeds * XM + (n_speeds * 5 + 15) / 8 + 1;   // per-pencil tables
+  double* meta = xtab + (long long)n_speeds * XM + (n_speeds + 1) / 2;   // per-pencil tables
 
   const long long wp = blockIdx.x / n_lg;
-  const int t0 = (int)(blockIdx.x - wp * n_lg) * lg;   // first line of the group
+  const int t0 = (int)(blockIdx.x - wp * n_lg) * LG;   // first line of the group
   const long long q = P.walk_pencils[wp];
   const long long off = P.p_off[q];
   const int n = P.p_n[q];
   const int lev = P.e_level[off];
   const int tid = threadIdx.x;
 
-  for (int k = tid; k < n_speeds * XM; k += blockDim.x) xtab[k] = __ldg(X.mats + k);
-  for (int k = tid; k < n_speeds; k += blockDim.x) {
-    xns[k] = (int)X.ns[k];
-    xid[k] = X.ident[k];
+  // x-shift tables; a zero shift is stored as (A, B) = (I, 0) with no cell shift so
+  // the X phases run without a per-thread branch (1*u0 + 0*u1 + ... == u0)
+  for (int k = tid; k < n_speeds * XM; k += blockDim.x) {
+    const int g = k / XM, e = k - g * XM;
+    xtab[k] = X.ident[g] ? ((e < OX * OX && e % (OX + 1) == 0) ? 1.0 : 0.0) : __ldg(X.mats + k);
   }
+  for (int k = tid; k < n_speeds; k += blockDim.x) xns[k] = X.ident[k] ? 0 : (int)X.ns[k];
   if (tid == 0) {
     s_nsmin = 1 << 30;
     s_nsmax = -(1 << 30);
@@ -122,9 +128,6 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   }
   double Av[OV * OV], Bv[OV * OV];
   if (colv) load_pair<OV>(lm_mats, lev, n_cols, c, Av, Bv);
-  const int cxc = colv ? c / OX : 0;
-  const bool ghostL = colv && cxc >= n_xc - hl;   // column also feeds the left ghost
-  const bool ghostR = colv && cxc < hr;           // ... and/or the right ghost
   __syncthreads();
   const bool streamable = (s_nsmin >= -1 && s_nsmax <= 0) || (s_nsmin > s_nsmax);
   const bool per = (bc == SLDG_BC_PERIODIC);
@@ -133,7 +136,6 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   const bool xv = tid < OV * n_xc;
   const int iv = xv ? tid / n_xc : 0;
   const int cx = xv ? tid - iv * n_xc : 0;
-  const bool xghL = xv && cx >= n_xc - hl, xghR = xv && cx < hr;
   double m0a[OX], m1a[OX], m2a[OX], rha[OX];
 #pragma unroll
   for (int k = 0; k < OX; ++k) m0a[k] = m1a[k] = m2a[k] = rha[k] = 0.0;
@@ -157,7 +159,6 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     m[R + r] = wr * __ldg(fa.v0 + row);
     m[2 * R + r] = wr * __ldg(fa.v2 + row);
   }
-  auto cell_row0 = [&](int s) -> long long { return crow[s]; };
   __syncthreads();
 
   // ---- ring of cell tiles (as k_sweep_stream)
@@ -168,14 +169,43 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     const int cell = v < 0 ? n - 1 : (v >= n ? 0 : v);
     unsigned long long* bar = &full[k % kFRing];
     mbar_expect_tx(bar, (unsigned)(tile * 8));
-    bulk_g2s(ring + (k % kFRing) * tile, fin + cell_row0(cell) * n_cols, (unsigned)(tile * 8), bar);
+    bulk_g2s(ring + (k % kFRing) * tile, fin + crow[cell] * n_cols, (unsigned)(tile * 8), bar);
   };
   if (streamable && tid == 0)
     for (int k = 0; k < min(3, n_load); ++k) issue(k);
 
+  // V phase of one column: rows t*OV+i of the source cells sa / sb -> stA column c.
+  // CHECKED: the source cells may lie outside the pencil (absorbing ends).
+  auto vcol = [&](const double* sa, const double* sb, bool va, bool vb, auto checked) {
+    constexpr bool CK = decltype(checked)::value;
+    double* out = stA + c;
+#pragma unroll
+    for (int t = 0; t < LG; ++t) {
+      double ua[OV], ub[OV], y[OV];
+#pragma unroll
+      for (int i = 0; i < OV; ++i) {
+        const int r = t * OV + i;
+        if (CK) {
+          ua[i] = va ? sa[r * n_cols] : 0.0;
+          ub[i] = vb ? sb[r * n_cols] : 0.0;
+        } else {
+          ua[i] = sa[r * n_cols];
+          ub[i] = sb[r * n_cols];
+        }
+      }
+      two_cell<OV>(Av, Bv, ua, ub, CK ? va : true, CK ? vb : true, y);
+#pragma unroll
+      for (int i = 0; i < OV; ++i) out[(t * OV + i) * rw] = y[i];
+    }
+  };
+  auto vcopy = [&](const double* me) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) stA[r * rw + c] = me[r * n_cols];
+  };
+
   for (int s = 0; s < n; ++s) {
     const double* mcur = cmeta + (long long)s * 3 * R;
-    const long long r0 = cell_row0(s);
+    const long long r0 = crow[s];
     const int g_cur = xv ? cg[s * OV + iv] : 0;
     // ===================== V: pencil sweep of cell s -> stA (rows of R, stride rw)
     if (streamable) {
@@ -184,52 +214,41 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       const int klo = max(s - 1 - v0c, 0), khi = min(s + 1 - v0c, n_load - 1);
       for (int k = klo; k <= khi; ++k)
         mbar_wait(&full[k & (kFRing - 1)], (unsigned)(((unsigned)k / kFRing) & 1));
-    }
-    if (colv) {
-      double* out = stA + c;
-      if (speed == 0.0) {
-        const double* me = streamable ? ring + ((s - v0c) & (kFRing - 1)) * tile + c
-                                      : fin + r0 * n_cols + c;
-        for (int r = 0; r < R; ++r) out[r * rw] = me[r * n_cols];
-      } else {
-        const int va_cell = s - (int)nsv, vb_cell = s - (int)nsv - 1;
-        bool va = true, vb = true;
-        const double *sa, *sb;
-        if (streamable) {
-          va = per || (va_cell >= 0 && va_cell < n);
-          vb = per || (vb_cell >= 0 && vb_cell < n);
-          sa = ring + (((va ? va_cell : s) - v0c) & (kFRing - 1)) * tile + c;
-          sb = ring + (((vb ? vb_cell : s) - v0c) & (kFRing - 1)) * tile + c;
+      if (colv) {
+        if (speed == 0.0) {
+          vcopy(ring + ((s - v0c) & (kFRing - 1)) * tile + c);
         } else {
-          long long qa = va_cell, qb = vb_cell;
-          if (per) {
-            qa = pymod(qa, n);
-            qb = pymod(qb, n);
+          // streamable: source cells s - nsv and s - nsv - 1 with nsv in {-1, 0}
+          const int va_cell = s - (int)nsv, vb_cell = va_cell - 1;
+          if (per || (s > 0 && s < n - 1)) {
+            vcol(ring + ((va_cell - v0c) & (kFRing - 1)) * tile + c,
+                 ring + ((vb_cell - v0c) & (kFRing - 1)) * tile + c, true, true, BoolC<false>{});
           } else {
-            va = qa >= 0 && qa < n;
-            vb = qb >= 0 && qb < n;
+            const bool va = va_cell >= 0 && va_cell < n, vb = vb_cell >= 0 && vb_cell < n;
+            vcol(ring + (((va ? va_cell : s) - v0c) & (kFRing - 1)) * tile + c,
+                 ring + (((vb ? vb_cell : s) - v0c) & (kFRing - 1)) * tile + c, va, vb,
+                 BoolC<true>{});
           }
-          sa = fin + cell_row0(va ? (int)qa : s) * n_cols + c;
-          sb = fin + cell_row0(vb ? (int)qb : s) * n_cols + c;
         }
-        for (int t = 0; t < lg; ++t) {
-          double ua[OV], ub[OV], y[OV];
-#pragma unroll
-          for (int i = 0; i < OV; ++i) {
-            ua[i] = va ? sa[i * n_cols] : 0.0;
-            ub[i] = vb ? sb[i * n_cols] : 0.0;
-          }
-          two_cell<OV>(Av, Bv, ua, ub, va, vb, y);
-#pragma unroll
-          for (int i = 0; i < OV; ++i) out[i * rw] = y[i];
-          sa += OV * n_cols;
-          sb += OV * n_cols;
-          out += OV * rw;
+      }
+    } else if (colv) {
+      if (speed == 0.0) {
+        vcopy(fin + r0 * n_cols + c);
+      } else {
+        long long qa = s - nsv, qb = s - nsv - 1;
+        bool va = true, vb = true;
+        if (per) {
+          qa = pymod(qa, n);
+          qb = pymod(qb, n);
+        } else {
+          va = qa >= 0 && qa < n;
+          vb = qb >= 0 && qb < n;
         }
+        vcol(fin + crow[va ? (int)qa : s] * n_cols + c, fin + crow[vb ? (int)qb : s] * n_cols + c,
+             va, vb, BoolC<true>{});
       }
     }
     // x shift of this thread's rows for cell s: matrices to registers, wrapped sources
-    const bool ident = xid[g_cur] != 0;
     double xa[OX * OX], xb[OX * OX];
     int ia = 0, ib = 0;
     if (xv) {
@@ -242,16 +261,10 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       ia = cx - xns[g_cur];
       ia = ia < 0 ? ia + n_xc : (ia >= n_xc ? ia - n_xc : ia);
       ib = ia == 0 ? n_xc - 1 : ia - 1;
-      if (ident) ia = cx;
       ia *= OX;
       ib *= OX;
     }
     auto xapply = [&](const double* srow, double* y) {
-      if (ident) {
-#pragma unroll
-        for (int k = 0; k < OX; ++k) y[k] = srow[ia + k];
-        return;
-      }
       double ua[OX], ub[OX];
 #pragma unroll
       for (int j = 0; j < OX; ++j) {
@@ -273,7 +286,8 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     __syncthreads();
     // ===================== X1 (trailing half step): stA -> stB, moments
     if (xv) {
-      for (int t = 0; t < lg; ++t) {
+#pragma unroll
+      for (int t = 0; t < LG; ++t) {
         const int r = t * OV + iv;
         double y[OX];
         xapply(stA + r * rw, y);
@@ -290,9 +304,12 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     }
     __syncthreads();
     // ===================== X2 (next step's leading half): stB -> HBM, rho
+    // No barrier after X2: the next V writes stA (last read in X1, before the
+    // barrier above) and the ring slot it refills was last read in this V.
     if (xv) {
       double* dst = fout + (r0 + iv) * n_cols + cx * OX;
-      for (int t = 0; t < lg; ++t) {
+#pragma unroll
+      for (int t = 0; t < LG; ++t) {
         const int r = t * OV + iv;
         double y[OX];
         xapply(stB + r * rw, y);
@@ -305,8 +322,9 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
         dst += (long long)OV * n_cols;
       }
     }
-    __syncthreads();   // ring slot of cell s-1, stA/stB and the meta buffer are reused next
   }
+  __syncthreads();   // stB (read by X2) is reused by the reduction below
+
 
   // ---- CTA partials: rho per column (over i_v in order), moments contracted with xw
   double* red = stA;   // reuse: OV x n_cols, then 3 x blockDim
@@ -367,15 +385,14 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   if (threads > 384) return no("fused step: rows wider than 384 columns");
   const int hl = (int)xp->halo_l, hr = (int)xp->halo_r;
   if (hl > xp->n_cells || hr > xp->n_cells) return no("fused step: shift wider than the row");
-  g.gl = 0;
   g.rw = (int)n_cols + (n_cols % 2 == 0 ? 1 : 0);   // odd row stride: conflict-free columns
   const size_t fixed = sizeof(double) * (size_t)xp->n_speeds * 2 * OX * OX +
-                       sizeof(double) * ((xp->n_speeds * 5 + 15) / 8 + 1) + 64;
+                       sizeof(double) * ((xp->n_speeds + 1) / 2) + 64;
   const size_t nmax = (size_t)vp->max_pencil_cells;
   const size_t budget = 227 * 1024 - 1024;
   g.lg = 0;
-  for (int lg = std::min(8, OV * OV); lg >= 1; --lg) {
-    if ((OV * OV) % lg) continue;
+  for (int lg = 4; lg >= 1; --lg) {   // instantiated line groups: OV, 2 (even OV), 1
+    if ((OV * OV) % lg || (lg != OV && lg != 2 && lg != 1)) continue;
     const size_t R = (size_t)lg * OV;
     const size_t tables = 8 * nmax + 4 * ((nmax * OV + 1) & ~(size_t)1) + 8 * nmax * 3 * R;
     const size_t smem = sizeof(double) * (kFRing * R * n_cols + 2 * R * g.rw) + fixed + tables;
@@ -397,18 +414,35 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   return g;
 }
 
+template <int OV, int OX, int LG>
+static int launch_fused_lg(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
+                           const double* fin, double* fout, long long n_cols,
+                           const double* speeds, int bc, const long long* lm_ns,
+                           const double* lm_mats, const FusedArgs& fa, cudaStream_t st) {
+  auto k = k_step_fused<OV, OX, LG>;
+  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  k<<<(unsigned)g.grid, g.threads, g.smem, st>>>(vp->dev, xp->dev, fin, fout, (int)n_cols,
+                                                 (int)xp->n_cells, speeds, bc, lm_ns, lm_mats,
+                                                 g.rw, (int)xp->n_speeds, fa);
+  SLDG_LAUNCH_CHECK("k_step_fused");
+  return SLDG_OK;
+}
+
 template <int OV, int OX>
 static int launch_fused(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
                         const double* fin, double* fout, long long n_cols, const double* speeds,
                         int bc, const long long* lm_ns, const double* lm_mats,
                         const FusedArgs& fa, cudaStream_t st) {
-  auto k = k_step_fused<OV, OX>;
-  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
-  k<<<(unsigned)g.grid, g.threads, g.smem, st>>>(
-      vp->dev, xp->dev, fin, fout, (int)n_cols, (int)xp->n_cells, speeds, bc, lm_ns, lm_mats,
-      g.lg, g.n_lg, (int)xp->halo_l, (int)xp->halo_r, g.gl, g.rw, (int)xp->n_speeds, fa);
-  SLDG_LAUNCH_CHECK("k_step_fused");
-  return SLDG_OK;
+  if (g.lg == OV)
+    return launch_fused_lg<OV, OX, OV>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st);
+  if constexpr (OV % 2 == 0 && OV != 2) {
+    if (g.lg == 2)
+      return launch_fused_lg<OV, OX, 2>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st);
+  }
+  if (g.lg == 1)
+    return launch_fused_lg<OV, OX, 1>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st);
+  set_error("fused step: no kernel for this line group");
+  return SLDG_ERR_UNSUPPORTED;
 }
 
 static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
