@@ -24,6 +24,7 @@ struct VPlanDev {
   const int* c_group;
   const double* c_weight;
   const long long* walk_pencils;  // whole-fast pencils, for k_sweep_walk
+  const long long* walk_desc;     // per walk position: {p_off, p_n | level << 32}
   const long long* gen_entries;   // entries handled by k_sweep_generic when walk is used
   long long n_entries, n_targets, n_walk, n_gen;
   int stride_d, stride_t0, stride_t1;
@@ -38,7 +39,7 @@ struct sldg_vplan {
   sldg::VPlanDev dev;
   int dim, direction, o, n_lines, n_local;
   long long n_cells, n_pencils, n_entries, n_slots, n_targets, n_walk, n_gen, n_dofs;
-  int max_pencil_cells;
+  int max_pencil_cells, max_walk_cells;
   void* block;
 };
 

@@ -6,22 +6,31 @@
 // field solve -> advect_velocity (vsweep.py:413-441) -> advect_x
 // (xfield.py:91-104) -> diagnostics (driver.py:220-229, moments 139-146), and
 // the next step starts with advect_x and compute_rho (xfield.py:107-109).
-// This kernel performs, for one pencil and a group of LG lines of its cells:
+// For every cell of a pencil and a group of LG lines of that cell (a "tile":
+// R = LG*OV rows spanning all x columns) the kernel performs
 //   V  : whole-pencil fast path (sweep_pencil, vsweep.py:197-200) from a TMA
 //        bulk-copy ring of cell tiles (as k_sweep_stream), into shared memory;
-//   X1 : trailing half x-step on the tile's rows (they are complete rows:
-//        the tile spans all x columns), moments of the result accumulated;
+//   X1 : trailing half x-step on the tile's rows (they are complete rows),
+//        moments of the result accumulated;
 //   X2 : leading half x-step of the next step, rho of the result accumulated,
 //        result stored to HBM.
 // Every coefficient is read once and written once per step: 16 B/DOF instead
 // of 32 B/DOF for the separate sweep and X.X passes.  Arithmetic per output is
 // the same as in k_sweep_stream / k_xadv (same operands, same order).
 //
+// Work decomposition: persistent CTAs (resident count x SMs).  The work is the
+// sequence of items (walk pencil, line group), each a run of cell tiles; CTA b
+// owns the contiguous tile range [b*T/G, (b+1)*T/G), so every CTA does the same
+// number of tiles (no tail wave) and items may be split between two CTAs (a
+// tile only needs its cell's neighbours, which the ring loads as well).  One
+// TMA ring runs across the CTA's items; the next item's tables (pencil
+// descriptor, tile rows, x-speed indices, row weights) are prefetched with
+// cp.async while the current item is computed, so there is no per-item
+// prologue on the critical path.
+//
 // Thread mappings: V phase thread = x column (its A, B for the pencil's level
 // in registers); X phases thread = (velocity node i_v, x cell): all rows of a
 // tile with the same i_v share one v_x, hence one x-shift and one A, B pair.
-// Shared-memory rows carry ghost cells on both sides so periodic x reads never
-// wrap (writers duplicate the edge cells into the ghosts).
 //
 // Eligible: dim 3, direction 0, every pencil whole-pencil-fast, no weighted
 // (1/n_c) entries, tile rows span the whole row (ld == n_cols).  Otherwise the
@@ -59,6 +68,7 @@ static __global__ void k_fold3(const double* __restrict__ part, long long n, dou
 }
 
 constexpr int kFRing = 4;
+constexpr int kMaxLev = 8;
 
 struct FusedArgs {
   const double* w;
@@ -72,18 +82,26 @@ struct FusedArgs {
 template <bool B>
 using BoolC = std::integral_constant<bool, B>;
 
+// per-item tables in shared memory (two buffers: current item, next item)
+struct ItemTabs {
+  long long* crow;   // [nmax] first row of each cell (line 0)
+  double* cm;        // [nmax][3][R] w, v0, v2 of the tile rows
+  int* cg;           // [nmax][OV] x-speed index per (cell, v_x node)
+};
+
 template <int OV, int OX, int LG>
 __global__ void __launch_bounds__(384, 1)
 k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout,
              int n_cols, int n_xc, const double* __restrict__ speeds, int bc,
              const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats, int rw,
-             int n_speeds, FusedArgs fa) {
+             int n_speeds, int nmax, long long n_tiles, FusedArgs fa) {
   constexpr int XM = 2 * OX * OX;
   constexpr int R = LG * OV;                    // rows per tile
   constexpr int n_lg = OV * OV / LG;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long full[kFRing];
-  __shared__ int s_nsmin, s_nsmax;
+  __shared__ int s_nsmin[kMaxLev], s_nsmax[kMaxLev];
+  __shared__ __align__(16) long long s_wd[2][2];   // walk descriptor per table buffer
 
   const int tile = R * n_cols;                  // doubles per ring slot
   double* ring = sm;
@@ -91,88 +109,160 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   double* stB = stA + R * rw;
   double* xtab = stB + R * rw;                  // n_speeds x (A|B) for the x shift
   int* xns = reinterpret_cast<int*>(xtab + (long long)n_speeds * XM);
-  double* meta = xtab + (long long)n_speeds * XM + (n_speeds + 1) / 2;   // per-pencil tables
+  double* xws = xtab + (long long)n_speeds * XM + (n_speeds + 1) / 2;   // x quadrature weights
+  double* tabs0 = xws + n_cols;
+  const int tab_dbl = nmax + 3 * R * nmax + (nmax * OV + 1) / 2;
+  auto tabs = [&](int b) -> ItemTabs {
+    double* base = tabs0 + (long long)b * tab_dbl;
+    return ItemTabs{reinterpret_cast<long long*>(base), base + nmax,
+                    reinterpret_cast<int*>(base + nmax + 3 * R * nmax)};
+  };
 
-  const long long wp = blockIdx.x / n_lg;
-  const int t0 = (int)(blockIdx.x - wp * n_lg) * LG;   // first line of the group
-  const long long q = P.walk_pencils[wp];
-  const long long off = P.p_off[q];
-  const int n = P.p_n[q];
-  const int lev = P.e_level[off];
   const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const long long tb = (long long)blockIdx.x * n_tiles / gridDim.x;
+  const long long te = (long long)(blockIdx.x + 1) * n_tiles / gridDim.x;
+  const long long it_first = tb / nmax, it_last = (te - 1) / nmax;   // item range (inclusive)
+  const int n_items = (int)(it_last - it_first + 1);
 
   // x-shift tables; a zero shift is stored as (A, B) = (I, 0) with no cell shift so
   // the X phases run without a per-thread branch (1*u0 + 0*u1 + ... == u0)
-  for (int k = tid; k < n_speeds * XM; k += blockDim.x) {
+  for (int k = tid; k < n_speeds * XM; k += nthr) {
     const int g = k / XM, e = k - g * XM;
     xtab[k] = X.ident[g] ? ((e < OX * OX && e % (OX + 1) == 0) ? 1.0 : 0.0) : __ldg(X.mats + k);
   }
-  for (int k = tid; k < n_speeds; k += blockDim.x) xns[k] = X.ident[k] ? 0 : (int)X.ns[k];
+  for (int k = tid; k < n_speeds; k += nthr) xns[k] = X.ident[k] ? 0 : (int)X.ns[k];
+  for (int k = tid; k < n_cols; k += nthr) xws[k] = __ldg(fa.xw + k);
+  if (tid < kMaxLev) {
+    s_nsmin[tid] = 1 << 30;
+    s_nsmax[tid] = -(1 << 30);
+  }
   if (tid == 0) {
-    s_nsmin = 1 << 30;
-    s_nsmax = -(1 << 30);
     for (int k = 0; k < kFRing; ++k) mbar_init(&full[k], 1);
     mbar_fence_init();
   }
   __syncthreads();
 
-  // ---- V-phase state: thread = column
+  // ---- V-phase state: thread = column; a level is streamable when every moving
+  // column's integer shift is -1 or 0 (sources in cells s-1, s, s+1)
   const bool colv = tid < n_cols;
   const int c = tid;
   const double speed = colv ? __ldg(speeds + c) : 0.0;
-  const long long nsv = colv ? lm_ns[(long long)lev * n_cols + c] : 0;
   if (colv && speed != 0.0) {
-    const int nsi = (int)max(min(nsv, (long long)(1 << 29)), -(long long)(1 << 29));
-    atomicMin(&s_nsmin, nsi);
-    atomicMax(&s_nsmax, nsi);
+    for (int L = 0; L < P.n_levels; ++L) {
+      const long long v = lm_ns[(long long)L * n_cols + c];
+      const int nsi = (int)max(min(v, (long long)(1 << 29)), -(long long)(1 << 29));
+      atomicMin(&s_nsmin[L], nsi);
+      atomicMax(&s_nsmax[L], nsi);
+    }
   }
-  double Av[OV * OV], Bv[OV * OV];
-  if (colv) load_pair<OV>(lm_mats, lev, n_cols, c, Av, Bv);
-  __syncthreads();
-  const bool streamable = (s_nsmin >= -1 && s_nsmax <= 0) || (s_nsmin > s_nsmax);
   const bool per = (bc == SLDG_BC_PERIODIC);
 
   // ---- X-phase state: thread = (iv, x cell)
   const bool xv = tid < OV * n_xc;
   const int iv = xv ? tid / n_xc : 0;
   const int cx = xv ? tid - iv * n_xc : 0;
-  double m0a[OX], m1a[OX], m2a[OX], rha[OX];
+  // moments: each output row is contracted with the x weights first, then
+  // weighted by (w, w*v0, w*v2); rho per x column
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0, rha[OX];
 #pragma unroll
-  for (int k = 0; k < OX; ++k) m0a[k] = m1a[k] = m2a[k] = rha[k] = 0.0;
+  for (int k = 0; k < OX; ++k) rha[k] = 0.0;
 
-  // per-pencil metadata, loaded once into shared memory (no global loads in the
-  // step loop): tile row base per cell, x-speed index per (cell, v_x node) and
-  // (w, w*v0, w*v2) per tile row of every cell
-  long long* crow = reinterpret_cast<long long*>(meta);                   // [n]
-  int* cg = reinterpret_cast<int*>(crow + n);                               // [n][OV]
-  double* cmeta = reinterpret_cast<double*>(cg + ((n * OV + 1) & ~1));      // [n][3][R]
-  for (int k = tid; k < n; k += blockDim.x) crow[k] = P.e_row0[off + k] + (long long)t0 * OV;
-  __syncthreads();
-  for (int k = tid; k < n * OV; k += blockDim.x)
-    cg[k] = __ldg(X.row_speed + crow[k / OV] + k % OV);
-  for (int k = tid; k < n * R; k += blockDim.x) {
-    const int s2 = k / R, r = k - s2 * R;
-    const long long row = crow[s2] + r;
-    const double wr = __ldg(fa.w + row);
-    double* m = cmeta + (long long)s2 * 3 * R;
-    m[r] = wr;
-    m[R + r] = wr * __ldg(fa.v0 + row);
-    m[2 * R + r] = wr * __ldg(fa.v2 + row);
-  }
-  __syncthreads();
-
-  // ---- ring of cell tiles (as k_sweep_stream)
-  const int v0c = per ? -1 : 0;
-  const int n_load = per ? n + 2 : n;
-  auto issue = [&](int k) {
-    const int v = v0c + k;
-    const int cell = v < 0 ? n - 1 : (v >= n ? 0 : v);
-    unsigned long long* bar = &full[k % kFRing];
-    mbar_expect_tx(bar, (unsigned)(tile * 8));
-    bulk_g2s(ring + (k % kFRing) * tile, fin + crow[cell] * n_cols, (unsigned)(tile * 8), bar);
+  // ---- item bookkeeping (uniform across the CTA)
+  auto item_wp = [&](long long it) { return it / n_lg; };
+  auto item_t0 = [&](long long it) { return (int)(it - (it / n_lg) * n_lg) * LG; };
+  auto item_sb = [&](long long it) { return (int)(it == it_first ? tb - it * nmax : 0); };
+  auto item_se = [&](long long it, int n) {
+    return (int)min((long long)n, te - it * nmax);   // exclusive, clipped to the pencil
   };
-  if (streamable && tid == 0)
-    for (int k = 0; k < min(3, n_load); ++k) issue(k);
+  auto wd_n = [&](int b) { return (int)(s_wd[b][1] & 0xffffffffLL); };
+  auto wd_lev = [&](int b) { return (int)(s_wd[b][1] >> 32); };
+  // prefetch stages of item `it` into table buffer b (cp.async, completed by the
+  // caller's cp_async_wait_all + __syncthreads before the next stage reads them)
+  auto stage = [&](int st, int b, long long it) {
+    const ItemTabs T = tabs(b);
+    if (st == 0) {
+      if (tid == 0) cp_async16(&s_wd[b][0], P.walk_desc + 2 * item_wp(it));
+    } else if (st == 1) {
+      const long long off = s_wd[b][0];
+      const int n = wd_n(b);
+      for (int k = tid; k < n; k += nthr) cp_async8(T.crow + k, P.e_row0 + off + k);
+    } else {
+      const int n = wd_n(b);
+      const long long l0 = (long long)item_t0(it) * OV;
+      for (int k = tid; k < n * OV; k += nthr)
+        cp_async4(T.cg + k, X.row_speed + T.crow[k / OV] + l0 + k % OV);
+      for (int k = tid; k < n * 3 * R; k += nthr) {
+        const int s2 = k / (3 * R), rem = k - s2 * 3 * R, a = rem / R, r = rem - a * R;
+        const double* src = a == 0 ? fa.w : (a == 1 ? fa.v0 : fa.v2);
+        cp_async8(T.cm + k, src + T.crow[s2] + l0 + r);
+      }
+    }
+  };
+  auto stage_sync = [&](int st, int b, long long it) {
+    stage(st, b, it);
+    cp_async_wait_all();
+    __syncthreads();
+  };
+
+  // item 0 tables, synchronously
+  for (int st = 0; st < 3; ++st) stage_sync(st, 0, it_first);
+
+  // ---- ring of cell tiles: one load sequence across the CTA's items.  Item i's
+  // loads are the cells first..last of its segment (sb-1..se, wrapped when
+  // periodic, clipped when absorbing); non-streamable items load nothing.
+  auto seg_first = [&](int sb) { return per ? sb - 1 : max(sb - 1, 0); };
+  auto seg_last = [&](int se, int n) { return per ? se : min(se, n - 1); };
+  // thread-0 issue cursor, kept in shared memory (no registers across the loop):
+  // item, next cell, last cell, loads issued, cursor initialised for the item
+  __shared__ int s_cur[5];
+  if (tid == 0) {
+    s_cur[0] = 0;
+    s_cur[1] = 0;
+    s_cur[2] = -1;
+    s_cur[3] = 0;
+    s_cur[4] = 0;
+  }
+  auto pump = [&](int limit, int cur_i, bool next_ready) {
+    int ld_i = s_cur[0], ld_c = s_cur[1], ld_last = s_cur[2], issued = s_cur[3];
+    bool ld_init = s_cur[4] != 0;
+    while (issued < limit && ld_i < n_items) {
+      if (ld_i > cur_i + 1 || (ld_i == cur_i + 1 && !next_ready)) break;
+      const int b = ld_i & 1;
+      const long long it = it_first + ld_i;
+      const int n = wd_n(b);
+      if (!ld_init) {
+        const int sb = item_sb(it), se = item_se(it, n);
+        const int lev = wd_lev(b);
+        const bool strm = (s_nsmin[lev] >= -1 && s_nsmax[lev] <= 0) || (s_nsmin[lev] > s_nsmax[lev]);
+        ld_c = seg_first(sb);
+        ld_last = (strm && se > sb) ? seg_last(se, n) : ld_c - 1;
+        ld_init = true;
+      }
+      if (ld_c > ld_last) {
+        ++ld_i;
+        ld_init = false;
+        continue;
+      }
+      const int cell = ld_c < 0 ? n - 1 : (ld_c >= n ? 0 : ld_c);
+      const long long row0 = tabs(b).crow[cell] + (long long)item_t0(it) * OV;
+      unsigned long long* bar = &full[issued & (kFRing - 1)];
+      mbar_expect_tx(bar, (unsigned)(tile * 8));
+      bulk_g2s(ring + (issued & (kFRing - 1)) * tile, fin + row0 * n_cols, (unsigned)(tile * 8), bar);
+      ++issued;
+      ++ld_c;
+    }
+    s_cur[0] = ld_i;
+    s_cur[1] = ld_c;
+    s_cur[2] = ld_last;
+    s_cur[3] = issued;
+    s_cur[4] = ld_init ? 1 : 0;
+  };
+
+  double Av[OV * OV], Bv[OV * OV];
+  long long nsv = 0;
+  int cur_lev = -1;
+  int base = 0;   // load index of the current item's first load
 
   // V phase of one column: rows t*OV+i of the source cells sa / sb -> stA column c.
   // CHECKED: the source cells may lie outside the pencil (absorbing ends).
@@ -203,128 +293,158 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     for (int r = 0; r < R; ++r) stA[r * rw + c] = me[r * n_cols];
   };
 
-  for (int s = 0; s < n; ++s) {
-    const double* mcur = cmeta + (long long)s * 3 * R;
-    const long long r0 = crow[s];
-    const int g_cur = xv ? cg[s * OV + iv] : 0;
-    // ===================== V: pencil sweep of cell s -> stA (rows of R, stride rw)
-    if (streamable) {
-      const int kn = s + 2 - v0c;
-      if (tid == 0 && kn < n_load && kn >= 3) issue(kn);
-      const int klo = max(s - 1 - v0c, 0), khi = min(s + 1 - v0c, n_load - 1);
-      for (int k = klo; k <= khi; ++k)
-        mbar_wait(&full[k & (kFRing - 1)], (unsigned)(((unsigned)k / kFRing) & 1));
+  for (int i = 0; i < n_items; ++i) {
+    const int b = i & 1;
+    const long long it = it_first + i;
+    const ItemTabs T = tabs(b);
+    const int n = wd_n(b), lev = wd_lev(b);
+    const int sb = item_sb(it), se = item_se(it, n);
+    const long long l0 = (long long)item_t0(it) * OV;
+    const bool streamable =
+        (s_nsmin[lev] >= -1 && s_nsmax[lev] <= 0) || (s_nsmin[lev] > s_nsmax[lev]);
+    const int first = seg_first(sb), last = seg_last(se, n);
+    if (lev != cur_lev) {
+      cur_lev = lev;
       if (colv) {
-        if (speed == 0.0) {
-          vcopy(ring + ((s - v0c) & (kFRing - 1)) * tile + c);
-        } else {
-          // streamable: source cells s - nsv and s - nsv - 1 with nsv in {-1, 0}
-          const int va_cell = s - (int)nsv, vb_cell = va_cell - 1;
-          if (per || (s > 0 && s < n - 1)) {
-            vcol(ring + ((va_cell - v0c) & (kFRing - 1)) * tile + c,
-                 ring + ((vb_cell - v0c) & (kFRing - 1)) * tile + c, true, true, BoolC<false>{});
+        load_pair<OV>(lm_mats, lev, n_cols, c, Av, Bv);
+        nsv = lm_ns[(long long)lev * n_cols + c];
+      }
+    }
+    const bool has_next = i + 1 < n_items;
+    int n_staged = 0;   // prefetch stages of the next item issued so far
+    for (int s = sb; s < se; ++s) {
+      const double* mcur = T.cm + (long long)s * 3 * R;
+      const long long r0 = T.crow[s] + l0;
+      const int g_cur = xv ? T.cg[s * OV + iv] : 0;
+      // ===================== V: pencil sweep of cell s -> stA (rows of R, stride rw)
+      if (streamable) {
+        const int klo = base + max(s - 1, first) - first, khi = base + min(s + 1, last) - first;
+        if (tid == 0) pump(klo + kFRing, i, n_staged >= 4);
+        for (int k = klo; k <= khi; ++k)
+          mbar_wait(&full[k & (kFRing - 1)], (unsigned)((k / kFRing) & 1));
+        if (colv) {
+          auto slot = [&](int cell) { return ring + ((base + cell - first) & (kFRing - 1)) * tile + c; };
+          if (speed == 0.0) {
+            vcopy(slot(s));
           } else {
-            const bool va = va_cell >= 0 && va_cell < n, vb = vb_cell >= 0 && vb_cell < n;
-            vcol(ring + (((va ? va_cell : s) - v0c) & (kFRing - 1)) * tile + c,
-                 ring + (((vb ? vb_cell : s) - v0c) & (kFRing - 1)) * tile + c, va, vb,
-                 BoolC<true>{});
+            // streamable: source cells s - nsv and s - nsv - 1 with nsv in {-1, 0}
+            const int va_cell = s - (int)nsv, vb_cell = va_cell - 1;
+            if (per || (s > 0 && s < n - 1)) {
+              vcol(slot(va_cell), slot(vb_cell), true, true, BoolC<false>{});
+            } else {
+              const bool va = va_cell >= 0 && va_cell < n, vb = vb_cell >= 0 && vb_cell < n;
+              vcol(slot(va ? va_cell : s), slot(vb ? vb_cell : s), va, vb, BoolC<true>{});
+            }
+          }
+        }
+      } else {
+        if (colv) {
+          if (speed == 0.0) {
+            vcopy(fin + r0 * n_cols + c);
+          } else {
+            long long qa = s - nsv, qb = s - nsv - 1;
+            bool va = true, vb = true;
+            if (per) {
+              qa = pymod(qa, n);
+              qb = pymod(qb, n);
+            } else {
+              va = qa >= 0 && qa < n;
+              vb = qb >= 0 && qb < n;
+            }
+            vcol(fin + (T.crow[va ? (int)qa : s] + l0) * n_cols + c,
+                 fin + (T.crow[vb ? (int)qb : s] + l0) * n_cols + c, va, vb, BoolC<true>{});
           }
         }
       }
-    } else if (colv) {
-      if (speed == 0.0) {
-        vcopy(fin + r0 * n_cols + c);
-      } else {
-        long long qa = s - nsv, qb = s - nsv - 1;
-        bool va = true, vb = true;
-        if (per) {
-          qa = pymod(qa, n);
-          qb = pymod(qb, n);
-        } else {
-          va = qa >= 0 && qa < n;
-          vb = qb >= 0 && qb < n;
+      // x shift of this thread's rows for cell s: matrices to registers, wrapped sources
+      double xa[OX * OX], xb[OX * OX];
+      int ia = 0, ib = 0;
+      if (xv) {
+        const double* AB = xtab + (long long)g_cur * XM;
+#pragma unroll
+        for (int k = 0; k < OX * OX; ++k) {
+          xa[k] = AB[k];
+          xb[k] = AB[OX * OX + k];
         }
-        vcol(fin + crow[va ? (int)qa : s] * n_cols + c, fin + crow[vb ? (int)qb : s] * n_cols + c,
-             va, vb, BoolC<true>{});
+        ia = cx - xns[g_cur];
+        ia = ia < 0 ? ia + n_xc : (ia >= n_xc ? ia - n_xc : ia);
+        ib = ia == 0 ? n_xc - 1 : ia - 1;
+        ia *= OX;
+        ib *= OX;
       }
-    }
-    // x shift of this thread's rows for cell s: matrices to registers, wrapped sources
-    double xa[OX * OX], xb[OX * OX];
-    int ia = 0, ib = 0;
-    if (xv) {
-      const double* AB = xtab + (long long)g_cur * XM;
+      auto xapply = [&](const double* srow, double* y) {
+        double ua[OX], ub[OX];
 #pragma unroll
-      for (int k = 0; k < OX * OX; ++k) {
-        xa[k] = AB[k];
-        xb[k] = AB[OX * OX + k];
-      }
-      ia = cx - xns[g_cur];
-      ia = ia < 0 ? ia + n_xc : (ia >= n_xc ? ia - n_xc : ia);
-      ib = ia == 0 ? n_xc - 1 : ia - 1;
-      ia *= OX;
-      ib *= OX;
-    }
-    auto xapply = [&](const double* srow, double* y) {
-      double ua[OX], ub[OX];
-#pragma unroll
-      for (int j = 0; j < OX; ++j) {
-        ua[j] = srow[ia + j];
-        ub[j] = srow[ib + j];
-      }
-#pragma unroll
-      for (int k = 0; k < OX; ++k) {
-        double sa = xa[k * OX] * ua[0];
-        double sb = xb[k * OX] * ub[0];
-#pragma unroll
-        for (int j = 1; j < OX; ++j) {
-          sa = fma(xa[k * OX + j], ua[j], sa);
-          sb = fma(xb[k * OX + j], ub[j], sb);
+        for (int j = 0; j < OX; ++j) {
+          ua[j] = srow[ia + j];
+          ub[j] = srow[ib + j];
         }
-        y[k] = sa + sb;
-      }
-    };
-    __syncthreads();
-    // ===================== X1 (trailing half step): stA -> stB, moments
-    if (xv) {
-#pragma unroll
-      for (int t = 0; t < LG; ++t) {
-        const int r = t * OV + iv;
-        double y[OX];
-        xapply(stA + r * rw, y);
-        const double wr = mcur[r], wv0 = mcur[R + r], wv2 = mcur[2 * R + r];
-        double* o = stB + r * rw + cx * OX;
 #pragma unroll
         for (int k = 0; k < OX; ++k) {
-          o[k] = y[k];
-          m0a[k] = fma(wr, y[k], m0a[k]);
-          m1a[k] = fma(wv0, y[k], m1a[k]);
-          m2a[k] = fma(wv2, y[k], m2a[k]);
+          double sa = xa[k * OX] * ua[0];
+          double sb2 = xb[k * OX] * ub[0];
+#pragma unroll
+          for (int j = 1; j < OX; ++j) {
+            sa = fma(xa[k * OX + j], ua[j], sa);
+            sb2 = fma(xb[k * OX + j], ub[j], sb2);
+          }
+          y[k] = sa + sb2;
+        }
+      };
+      // prefetch stage copies issued at the previous step complete before this barrier
+      if (n_staged > 0 && n_staged <= 3) cp_async_wait_all();
+      __syncthreads();
+      if (has_next && n_staged < 3) stage(n_staged, b ^ 1, it + 1);
+      ++n_staged;
+      // ===================== X1 (trailing half step): stA -> stB, moments
+      if (xv) {
+#pragma unroll
+        for (int t = 0; t < LG; ++t) {
+          const int r = t * OV + iv;
+          double y[OX];
+          xapply(stA + r * rw, y);
+          const double wr = mcur[r], wv0 = wr * mcur[R + r], wv2 = wr * mcur[2 * R + r];
+          double* o = stB + r * rw + cx * OX;
+          double z = xws[cx * OX] * y[0];
+#pragma unroll
+          for (int k = 1; k < OX; ++k) z = fma(xws[cx * OX + k], y[k], z);
+#pragma unroll
+          for (int k = 0; k < OX; ++k) o[k] = y[k];
+          m0 = fma(wr, z, m0);
+          m1 = fma(wv0, z, m1);
+          m2 = fma(wv2, z, m2);
+        }
+      }
+      __syncthreads();
+      // ===================== X2 (next step's leading half): stB -> HBM, rho
+      // No barrier after X2: the next V writes stA (last read in X1, before the
+      // barrier above) and the ring slot it refills was last read in this V.
+      if (xv) {
+        double* dst = fout + (r0 + iv) * n_cols + cx * OX;
+#pragma unroll
+        for (int t = 0; t < LG; ++t) {
+          const int r = t * OV + iv;
+          double y[OX];
+          xapply(stB + r * rw, y);
+          const double wr = mcur[r];
+#pragma unroll
+          for (int k = 0; k < OX; ++k) {
+            dst[k] = y[k];
+            rha[k] = fma(wr, y[k], rha[k]);
+          }
+          dst += (long long)OV * n_cols;
         }
       }
     }
-    __syncthreads();
-    // ===================== X2 (next step's leading half): stB -> HBM, rho
-    // No barrier after X2: the next V writes stA (last read in X1, before the
-    // barrier above) and the ring slot it refills was last read in this V.
-    if (xv) {
-      double* dst = fout + (r0 + iv) * n_cols + cx * OX;
-#pragma unroll
-      for (int t = 0; t < LG; ++t) {
-        const int r = t * OV + iv;
-        double y[OX];
-        xapply(stB + r * rw, y);
-        const double wr = mcur[r];
-#pragma unroll
-        for (int k = 0; k < OX; ++k) {
-          dst[k] = y[k];
-          rha[k] = fma(wr, y[k], rha[k]);
-        }
-        dst += (long long)OV * n_cols;
-      }
+    if (streamable && se > sb) base += last - first + 1;
+    if (has_next) {
+      // finish the next item's prefetch when this segment was too short to hide it
+      if (n_staged >= 1 && n_staged <= 3) cp_async_wait_all();
+      __syncthreads();   // also: the next item overwrites nothing this one still reads
+      for (int st = max(n_staged, 0); st < 3; ++st) stage_sync(st, b ^ 1, it + 1);
     }
   }
   __syncthreads();   // stB (read by X2) is reused by the reduction below
-
 
   // ---- CTA partials: rho per column (over i_v in order), moments contracted with xw
   double* red = stA;   // reuse: OV x n_cols, then 3 x blockDim
@@ -339,34 +459,35 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     fa.rho_part[(long long)blockIdx.x * n_cols + c] = s;
   }
   __syncthreads();
-  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  if (xv) {
-#pragma unroll
-    for (int k = 0; k < OX; ++k) {
-      const double xwk = __ldg(fa.xw + cx * OX + k);
-      s0 = fma(xwk, m0a[k], s0);
-      s1 = fma(xwk, m1a[k], s1);
-      s2 = fma(xwk, m2a[k], s2);
-    }
-  }
-  red[tid] = s0;
-  red[blockDim.x + tid] = s1;
-  red[2 * blockDim.x + tid] = s2;
+  red[tid] = m0;
+  red[nthr + tid] = m1;
+  red[2 * nthr + tid] = m2;
   __syncthreads();
   if (tid < 3) {
     double s = 0.0;
-    for (int k = 0; k < (int)blockDim.x; ++k) s += red[tid * blockDim.x + k];
+    for (int k = 0; k < nthr; ++k) s += red[tid * nthr + k];
     fa.mom_part[blockIdx.x * 3 + tid] = s;
   }
 }
 
 struct FusedGeom {
   bool ok;
-  int lg, n_lg, gl, rw, threads;
+  int lg, n_lg, rw, threads, nmax;
   size_t smem;
-  long long grid;
+  long long grid, n_tiles;
   std::string why;
 };
+
+static int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
 
 static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long long n_cols,
                             long long ld) {
@@ -379,6 +500,8 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   };
   if (vp->dim != 3 || vp->direction != 0) return no("fused step: dim 3, direction 0 only");
   if (vp->n_gen != 0 || vp->n_slots != 0) return no("fused step: AMR boundary / weighted entries");
+  if (vp->n_walk == 0) return no("fused step: no pencils");
+  if (vp->dev.n_levels > kMaxLev) return no("fused step: too many levels");
   if (ld != n_cols || n_cols != xp->n_cells * OX) return no("fused step: whole rows only");
   if (OV < 2 || OV > 4 || OX < 2 || OX > 4) return no("fused step: degrees 1..3");
   const long long threads = std::max<long long>(n_cols, OV * xp->n_cells);
@@ -386,15 +509,16 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   const int hl = (int)xp->halo_l, hr = (int)xp->halo_r;
   if (hl > xp->n_cells || hr > xp->n_cells) return no("fused step: shift wider than the row");
   g.rw = (int)n_cols + (n_cols % 2 == 0 ? 1 : 0);   // odd row stride: conflict-free columns
+  g.nmax = vp->max_walk_cells;
   const size_t fixed = sizeof(double) * (size_t)xp->n_speeds * 2 * OX * OX +
-                       sizeof(double) * ((xp->n_speeds + 1) / 2) + 64;
-  const size_t nmax = (size_t)vp->max_pencil_cells;
+                       sizeof(double) * ((xp->n_speeds + 1) / 2 + n_cols) + 64;
+  const size_t nmax = (size_t)g.nmax;
   const size_t budget = 227 * 1024 - 1024;
   g.lg = 0;
   for (int lg = 4; lg >= 1; --lg) {   // instantiated line groups: OV, 2 (even OV), 1
     if ((OV * OV) % lg || (lg != OV && lg != 2 && lg != 1)) continue;
     const size_t R = (size_t)lg * OV;
-    const size_t tables = 8 * nmax + 4 * ((nmax * OV + 1) & ~(size_t)1) + 8 * nmax * 3 * R;
+    const size_t tables = 2 * sizeof(double) * (nmax + 3 * R * nmax + (nmax * OV + 1) / 2);
     const size_t smem = sizeof(double) * (kFRing * R * n_cols + 2 * R * g.rw) + fixed + tables;
     const size_t red = sizeof(double) * std::max<size_t>(OV * n_cols, 3 * threads);
     if (smem <= budget && sizeof(double) * 2 * R * g.rw >= red) {
@@ -409,7 +533,10 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   if (g.lg == 0) return no("fused step: tile does not fit in shared memory");
   g.n_lg = OV * OV / g.lg;
   g.threads = (int)((threads + 31) / 32 * 32);
-  g.grid = vp->n_walk * g.n_lg;
+  g.n_tiles = vp->n_walk * g.n_lg * (long long)g.nmax;
+  // upper bound on the persistent grid (partials are sized for it); the launch
+  // clamps it to the resident CTA count
+  g.grid = std::min<long long>(g.n_tiles, 2LL * sm_count());
   g.ok = true;
   return g;
 }
@@ -418,13 +545,18 @@ template <int OV, int OX, int LG>
 static int launch_fused_lg(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
                            const double* fin, double* fout, long long n_cols,
                            const double* speeds, int bc, const long long* lm_ns,
-                           const double* lm_mats, const FusedArgs& fa, cudaStream_t st) {
+                           const double* lm_mats, const FusedArgs& fa, cudaStream_t st,
+                           long long* grid_out) {
   auto k = k_step_fused<OV, OX, LG>;
   SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
-  k<<<(unsigned)g.grid, g.threads, g.smem, st>>>(vp->dev, xp->dev, fin, fout, (int)n_cols,
-                                                 (int)xp->n_cells, speeds, bc, lm_ns, lm_mats,
-                                                 g.rw, (int)xp->n_speeds, fa);
+  int per_sm = 0;
+  SLDG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, g.threads, g.smem));
+  const long long grid = std::max<long long>(1, std::min<long long>(g.grid, (long long)std::max(per_sm, 1) * sm_count()));
+  k<<<(unsigned)grid, g.threads, g.smem, st>>>(vp->dev, xp->dev, fin, fout, (int)n_cols,
+                                               (int)xp->n_cells, speeds, bc, lm_ns, lm_mats,
+                                               g.rw, (int)xp->n_speeds, g.nmax, g.n_tiles, fa);
   SLDG_LAUNCH_CHECK("k_step_fused");
+  *grid_out = grid;
   return SLDG_OK;
 }
 
@@ -432,15 +564,18 @@ template <int OV, int OX>
 static int launch_fused(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
                         const double* fin, double* fout, long long n_cols, const double* speeds,
                         int bc, const long long* lm_ns, const double* lm_mats,
-                        const FusedArgs& fa, cudaStream_t st) {
+                        const FusedArgs& fa, cudaStream_t st, long long* grid_out) {
   if (g.lg == OV)
-    return launch_fused_lg<OV, OX, OV>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st);
+    return launch_fused_lg<OV, OX, OV>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats,
+                                       fa, st, grid_out);
   if constexpr (OV % 2 == 0 && OV != 2) {
     if (g.lg == 2)
-      return launch_fused_lg<OV, OX, 2>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st);
+      return launch_fused_lg<OV, OX, 2>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats,
+                                        fa, st, grid_out);
   }
   if (g.lg == 1)
-    return launch_fused_lg<OV, OX, 1>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st);
+    return launch_fused_lg<OV, OX, 1>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats,
+                                      fa, st, grid_out);
   set_error("fused step: no kernel for this line group");
   return SLDG_ERR_UNSUPPORTED;
 }
@@ -504,20 +639,22 @@ int sldg_step_fused(const sldg_vplan* vp, const sldg_xplan* xp, const double* fi
   int rc = sldg_level_matrices(vp, speeds, n_cols, dt, (int64_t*)lm_ns, lm_frac, lm_mats, stream);
   if (rc) return rc;
   FusedArgs fa{w, v0, v2, xw, mom_part, rho_part};
+  long long grid = 0;
   rc = SLDG_ERR_UNSUPPORTED;
   switch (vp->o * 10 + xp->o) {
 #define CASE(A, B)                                                                          \
   case A * 10 + B:                                                                          \
-    rc = launch_fused<A, B>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st); \
+    rc = launch_fused<A, B>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st, \
+                            &grid);                                                         \
     break;
     CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(4, 2) CASE(4, 3)
     CASE(4, 4)
 #undef CASE
   }
   if (rc) return rc;
-  k_fold3<<<1, 96, 0, st>>>(mom_part, g.grid, mom_out3);
+  k_fold3<<<1, 96, 0, st>>>(mom_part, grid, mom_out3);
   SLDG_LAUNCH_CHECK("k_fold3");
-  k_fold_cols<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>(rho_part, g.grid, n_cols,
+  k_fold_cols<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>(rho_part, grid, n_cols,
                                                                       rho_out);
   SLDG_LAUNCH_CHECK("k_fold_cols");
   return SLDG_OK;

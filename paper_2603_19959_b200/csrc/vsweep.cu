@@ -514,11 +514,17 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
       set_error("cell mixes unit and fractional weights");
       return SLDG_ERR_PLAN;
     }
-  std::vector<long long> walk, gen;
+  std::vector<long long> walk, gen, walk_desc;
+  int max_walk = 0;
   for (long long q = 0; q < P; ++q) {
-    if (p_fast[q]) walk.push_back(q);
-    else
+    if (p_fast[q]) {
+      walk.push_back(q);
+      walk_desc.push_back(p_off[q]);
+      walk_desc.push_back((long long)p_n[q] | ((long long)e_level[p_off[q]] << 32));
+      max_walk = std::max(max_walk, p_n[q]);
+    } else {
       for (long long e = p_off[q]; e < p_off[q] + p_n[q]; ++e) gen.push_back(e);
+    }
   }
   const long long T = (long long)t_row0.size();
   const long long K = (long long)c_slot.size();
@@ -549,6 +555,7 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
       {c_group.data(), sizeof(int) * K, (void**)&p->dev.c_group},
       {c_weight.data(), sizeof(double) * K, (void**)&p->dev.c_weight},
       {walk.data(), sizeof(long long) * walk.size(), (void**)&p->dev.walk_pencils},
+      {walk_desc.data(), sizeof(long long) * walk_desc.size(), (void**)&p->dev.walk_desc},
       {gen.data(), sizeof(long long) * gen.size(), (void**)&p->dev.gen_entries},
   };
   size_t total = 0;
@@ -589,6 +596,7 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
   p->n_gen = (long long)gen.size();
   p->n_dofs = d->n_cells * nloc;
   p->max_pencil_cells = max_cells;
+  p->max_walk_cells = max_walk;
   int pw[3] = {1, o, o * o};
   int td[2];
   int k = 0;
