@@ -89,12 +89,17 @@ struct ItemTabs {
   int* cg;           // [nmax][OV] x-speed index per (cell, v_x node)
 };
 
-template <int OV, int OX, int LG>
+// NXC > 0: the row length (x cells) is a compile-time constant, so every shared
+// memory offset folds into the instruction (the headline configuration)
+template <int OV, int OX, int LG, int NXC>
 __global__ void __launch_bounds__(384, 1)
 k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout,
-             int n_cols, int n_xc, const double* __restrict__ speeds, int bc,
-             const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats, int rw,
+             int n_cols_arg, int n_xc_arg, const double* __restrict__ speeds, int bc,
+             const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats, int rw_arg,
              int n_speeds, int nmax, long long n_tiles, FusedArgs fa) {
+  const int n_xc = NXC > 0 ? NXC : n_xc_arg;
+  const int n_cols = NXC > 0 ? OX * NXC : n_cols_arg;
+  const int rw = NXC > 0 ? ((OX * NXC) | 1) : rw_arg;
   constexpr int XM = 2 * OX * OX;
   constexpr int R = LG * OV;                    // rows per tile
   constexpr int n_lg = OV * OV / LG;
@@ -547,7 +552,10 @@ static int launch_fused_lg(const sldg_vplan* vp, const sldg_xplan* xp, const Fus
                            const double* speeds, int bc, const long long* lm_ns,
                            const double* lm_mats, const FusedArgs& fa, cudaStream_t st,
                            long long* grid_out) {
-  auto k = k_step_fused<OV, OX, LG>;
+  auto k = k_step_fused<OV, OX, LG, 0>;
+  if constexpr (OV == 3 && OX == 3 && LG == 3) {
+    if (xp->n_cells == 64) k = k_step_fused<OV, OX, LG, 64>;
+  }
   SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
   int per_sm = 0;
   SLDG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, g.threads, g.smem));
