@@ -546,53 +546,262 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   return g;
 }
 
-template <int OV, int OX, int LG>
-static int launch_fused_lg(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
-                           const double* fin, double* fout, long long n_cols,
-                           const double* speeds, int bc, const long long* lm_ns,
-                           const double* lm_mats, const FusedArgs& fa, cudaStream_t st,
-                           long long* grid_out) {
-  auto k = k_step_fused<OV, OX, LG, 0>;
-  if constexpr (OV == 3 && OX == 3 && LG == 3) {
-    if (xp->n_cells == 64) k = k_step_fused<OV, OX, LG, 64>;
+using FusedKernel = void (*)(VPlanDev, XPlanDev, const double*, double*, int, int, const double*,
+                             int, const long long*, const double*, int, int, int, long long,
+                             FusedArgs);
+
+template <int OV, int OX>
+static FusedKernel pick_kernel(int lg, long long n_xc) {
+  if (lg == OV) {
+    if constexpr (OV == 3 && OX == 3) {
+      if (n_xc == 64) return k_step_fused<3, 3, 3, 64>;
+    }
+    return k_step_fused<OV, OX, OV, 0>;
   }
+  if constexpr (OV % 2 == 0 && OV != 2) {
+    if (lg == 2) return k_step_fused<OV, OX, 2, 0>;
+  }
+  if (lg == 1) return k_step_fused<OV, OX, 1, 0>;
+  return nullptr;
+}
+
+static FusedKernel fused_kernel(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g) {
+  switch (vp->o * 10 + xp->o) {
+#define CASE(A, B) \
+  case A * 10 + B: return pick_kernel<A, B>(g.lg, xp->n_cells);
+    CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(4, 2) CASE(4, 3)
+    CASE(4, 4)
+#undef CASE
+  }
+  return nullptr;
+}
+
+// resident persistent grid (deterministic for a device): partial rows written
+static int fused_grid(FusedKernel k, const FusedGeom& g, long long* grid) {
   SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
   int per_sm = 0;
   SLDG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, g.threads, g.smem));
-  const long long grid = std::max<long long>(1, std::min<long long>(g.grid, (long long)std::max(per_sm, 1) * sm_count()));
-  k<<<(unsigned)grid, g.threads, g.smem, st>>>(vp->dev, xp->dev, fin, fout, (int)n_cols,
-                                               (int)xp->n_cells, speeds, bc, lm_ns, lm_mats,
-                                               g.rw, (int)xp->n_speeds, g.nmax, g.n_tiles, fa);
-  SLDG_LAUNCH_CHECK("k_step_fused");
-  *grid_out = grid;
+  *grid = std::max<long long>(1, std::min<long long>(g.grid, (long long)std::max(per_sm, 1) * sm_count()));
   return SLDG_OK;
-}
-
-template <int OV, int OX>
-static int launch_fused(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
-                        const double* fin, double* fout, long long n_cols, const double* speeds,
-                        int bc, const long long* lm_ns, const double* lm_mats,
-                        const FusedArgs& fa, cudaStream_t st, long long* grid_out) {
-  if (g.lg == OV)
-    return launch_fused_lg<OV, OX, OV>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats,
-                                       fa, st, grid_out);
-  if constexpr (OV % 2 == 0 && OV != 2) {
-    if (g.lg == 2)
-      return launch_fused_lg<OV, OX, 2>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats,
-                                        fa, st, grid_out);
-  }
-  if (g.lg == 1)
-    return launch_fused_lg<OV, OX, 1>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats,
-                                      fa, st, grid_out);
-  set_error("fused step: no kernel for this line group");
-  return SLDG_ERR_UNSUPPORTED;
 }
 
 static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
+// scratch of the fused step: level matrices, then the CTA partials
+struct FusedScratch {
+  long long* lm_ns;
+  double *lm_frac, *lm_mats, *mom_part, *rho_part;
+  size_t bytes;
+};
+static FusedScratch fused_scratch(const sldg_vplan* vp, const FusedGeom& g, long long n_cols,
+                                  void* base) {
+  FusedScratch s{};
+  unsigned char* sb = (unsigned char*)base;
+  const size_t nl = (size_t)vp->dev.n_levels;
+  size_t o = 0;
+  s.lm_ns = (long long*)(sb + o);
+  o += al256(sizeof(long long) * nl * n_cols);
+  s.lm_frac = (double*)(sb + o);
+  o += al256(sizeof(double) * nl * n_cols);
+  s.lm_mats = (double*)(sb + o);
+  o += al256(sizeof(double) * nl * 2 * vp->o * vp->o * n_cols);
+  s.mom_part = (double*)(sb + o);
+  o += al256(sizeof(double) * g.grid * 3);
+  s.rho_part = (double*)(sb + o);
+  o += al256(sizeof(double) * g.grid * n_cols);
+  s.bytes = o;
+  return s;
+}
+
+// The field work between two fused steps in one single-CTA launch (1024
+// threads), each stage with the same per-element arithmetic and reduction order
+// as its stand-alone kernel, so the results are bitwise identical:
+//   [k_fold_cols, k_fold3] -> k_poisson_rhs -> k_gemv -> k_efield ->
+//   k_field_diag, k_level_mats.
+template <int O>
+__global__ void __launch_bounds__(1024, 1)
+k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_part,
+              const double* __restrict__ mom_part, long long n_parts,
+              double* __restrict__ mom_prev, double* __restrict__ rho, const double* __restrict__ pxw,
+              const double* __restrict__ green, const double* __restrict__ diff,
+              long long n_cells, int p, double length, double h, double* __restrict__ b,
+              double* __restrict__ phi, double* __restrict__ e, double* __restrict__ diag2,
+              DevBasis vb, double dt, double base_width, int n_levels,
+              long long* __restrict__ lm_ns, double* __restrict__ lm_frac,
+              double* __restrict__ lm_mats) {
+  constexpr int CH = 64;   // columns per fold chunk
+  __shared__ double red[1024], red2[1024];
+  __shared__ double fsm[32 * (CH + 1)];
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, nw = blockDim.x >> 5;
+  const int o = p + 1;
+  const long long n_dofs = n_cells * o, n_nodes = n_cells * p;
+  const double* r = rho_in;
+  if (!r) {
+    // fold the previous fused step's partials in k_fold_cols' order (lane l sums
+    // parts l, l+32, ...; then the xor butterfly), with coalesced loads: thread
+    // (l, column) forms lane l's sum, a warp per column does the butterfly
+    for (long long c0 = 0; c0 < n_dofs; c0 += CH) {
+      const int nc = (int)min((long long)CH, n_dofs - c0);
+      for (int idx = tid; idx < 32 * nc; idx += blockDim.x) {
+        const int l = idx / nc, cc = idx - l * nc;
+        double s = 0.0;
+        for (long long k = l; k < n_parts; k += 32) s += rho_part[k * n_dofs + c0 + cc];
+        fsm[l * (CH + 1) + cc] = s;
+      }
+      __syncthreads();
+      for (int cc = wp; cc < nc; cc += nw) {
+        double s = fsm[lane * (CH + 1) + cc];
+#pragma unroll
+        for (int of = 16; of > 0; of >>= 1) s += __shfl_xor_sync(0xffffffffu, s, of);
+        if (lane == 0) rho[c0 + cc] = s;
+      }
+      __syncthreads();
+    }
+    if (mom_prev && wp < 3) {
+      double s = 0.0;
+      for (long long k = lane; k < n_parts; k += 32) s += mom_part[k * 3 + wp];
+#pragma unroll
+      for (int of = 16; of > 0; of >>= 1) s += __shfl_xor_sync(0xffffffffu, s, of);
+      if (lane == 0) mom_prev[wp] = s;
+    }
+    __syncthreads();
+    r = rho;
+  }
+  // Poisson right-hand side (k_poisson_rhs)
+  double s = 0.0;
+  for (long long k = tid; k < n_dofs; k += blockDim.x) s = fma(pxw[k], r[k], s);
+  red[tid] = s;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (tid < st) red[tid] += red[tid + st];
+    __syncthreads();
+  }
+  const double rbar = red[0] / length;
+  for (long long node = tid; node < n_nodes; node += blockDim.x) {
+    const long long cell = node / p;
+    const int j = (int)(node - cell * p);
+    double v;
+    if (j == 0) {
+      const long long kprev = (cell == 0 ? n_cells - 1 : cell - 1) * o + p;
+      const long long kthis = cell * o;
+      const double cprev = __dmul_rn(pxw[kprev], __dsub_rn(r[kprev], rbar));
+      const double cthis = __dmul_rn(pxw[kthis], __dsub_rn(r[kthis], rbar));
+      v = (cell == 0) ? __dadd_rn(cthis, cprev) : __dadd_rn(cprev, cthis);
+    } else {
+      const long long k = cell * o + j;
+      v = __dmul_rn(pxw[k], __dsub_rn(r[k], rbar));
+    }
+    b[node] = v;
+  }
+  __syncthreads();
+  // phi = G b (k_gemv: warp per row)
+  for (long long row = wp; row < n_nodes; row += nw) {
+    double t = 0.0;
+    for (long long k = lane; k < n_nodes; k += 32) t = fma(__ldg(green + row * n_nodes + k), b[k], t);
+#pragma unroll
+    for (int of = 16; of > 0; of >>= 1) t += __shfl_xor_sync(0xffffffffu, t, of);
+    if (lane == 0) phi[row] = t;
+  }
+  __syncthreads();
+  // E (k_efield)
+  const double sc = -(2.0 / h);
+  for (long long k = tid; k < n_dofs; k += blockDim.x) {
+    const long long cell = k / o;
+    const int i = (int)(k - cell * o);
+    double t = 0.0;
+    for (int j = 0; j < o; ++j) {
+      const long long node = (cell * p + j) % n_nodes;
+      t = fma(__dmul_rn(sc, phi[node]), diff[i * o + j], t);
+    }
+    e[k] = t;
+  }
+  __syncthreads();
+  // field diagnostics (k_field_diag) and level matrices for speeds = E (k_level_mats)
+  double m = 0.0, q = 0.0;
+  for (long long k = tid; k < n_dofs; k += blockDim.x) {
+    const double v = e[k];
+    m = fmax(m, fabs(v));
+    q = fma(pxw[k], v * v, q);
+  }
+  red[tid] = m;
+  red2[tid] = q;
+  for (long long idx = tid; idx < n_dofs * n_levels; idx += blockDim.x) {
+    const int lev = (int)(idx / n_dofs);
+    const long long c = idx - (long long)lev * n_dofs;
+    const double width = base_width / (double)(1LL << lev);
+    long long ns;
+    double a;
+    split_shift(e[c], dt, width, &ns, &a);
+    double A[O * O], B[O * O];
+    overlap_pair<O>(vb, a, A, B);
+    lm_ns[idx] = ns;
+    lm_frac[idx] = a;
+#pragma unroll
+    for (int k = 0; k < O * O; ++k) {
+      lm_mats[((long long)(lev * 2 + 0) * O * O + k) * n_dofs + c] = A[k];
+      lm_mats[((long long)(lev * 2 + 1) * O * O + k) * n_dofs + c] = B[k];
+    }
+  }
+  __syncthreads();
+  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
+    if (tid < st) {
+      red[tid] = fmax(red[tid], red[tid + st]);
+      red2[tid] += red2[tid + st];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    diag2[0] = red[0];
+    diag2[1] = 0.5 * red2[0];
+  }
+}
+
 }  // namespace sldg
 
 using namespace sldg;
+
+
+namespace {
+
+int check_geom(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_cols, int64_t ld,
+               FusedGeom* g) {
+  *g = fused_geom(vp, xp, n_cols, ld);
+  if (!g->ok) {
+    set_error(g->why);
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  return SLDG_OK;
+}
+
+int launch_step(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g, const double* fin,
+                double* fout, int64_t n_cols, const double* speeds, int32_t bc,
+                const FusedScratch& s, const FusedArgs& fa, cudaStream_t st, long long* grid) {
+  if ((((unsigned long long)fin) & 15) != 0 || n_cols % 2 != 0) {
+    set_error("fused step: 16-byte aligned rows required");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  FusedKernel k = fused_kernel(vp, xp, g);
+  if (!k) {
+    set_error("fused step: no kernel for this degree / line group");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  int rc = fused_grid(k, g, grid);
+  if (rc) return rc;
+  k<<<(unsigned)*grid, g.threads, g.smem, st>>>(vp->dev, xp->dev, fin, fout, (int)n_cols,
+                                                (int)xp->n_cells, speeds, bc, s.lm_ns, s.lm_mats,
+                                                g.rw, (int)xp->n_speeds, g.nmax, g.n_tiles, fa);
+  SLDG_LAUNCH_CHECK("k_step_fused");
+  return SLDG_OK;
+}
+
+bool bad_step_args(const sldg_vplan* vp, const sldg_xplan* xp, const double* fin,
+                   const double* fout, const double* speeds, int32_t bc, const double* w,
+                   const double* v0, const double* v2, const double* xw, const void* scratch) {
+  return !vp || !xp || !fin || !fout || fin == fout || !speeds || !w || !v0 || !v2 || !xw ||
+         !scratch || (bc != SLDG_BC_PERIODIC && bc != SLDG_BC_ABSORBING);
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -602,15 +811,10 @@ int sldg_step_fused_query(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_
     set_error("null argument");
     return SLDG_ERR_ARG;
   }
-  FusedGeom g = fused_geom(vp, xp, n_cols, ld);
-  if (!g.ok) {
-    set_error(g.why);
-    return SLDG_ERR_UNSUPPORTED;
-  }
-  const size_t lm = al256(sizeof(long long) * vp->dev.n_levels * n_cols) +
-                    al256(sizeof(double) * vp->dev.n_levels * n_cols) +
-                    al256(sizeof(double) * vp->dev.n_levels * 2 * vp->o * vp->o * n_cols);
-  *scratch_bytes = lm + al256(sizeof(double) * g.grid * 3) + al256(sizeof(double) * g.grid * n_cols);
+  FusedGeom g;
+  int rc = check_geom(vp, xp, n_cols, ld, &g);
+  if (rc) return rc;
+  *scratch_bytes = fused_scratch(vp, g, n_cols, nullptr).bytes;
   return SLDG_OK;
 }
 
@@ -618,53 +822,87 @@ int sldg_step_fused(const sldg_vplan* vp, const sldg_xplan* xp, const double* fi
                     int64_t ld, int64_t n_cols, const double* speeds, double dt, int32_t bc,
                     const double* w, const double* v0, const double* v2, const double* xw,
                     double* mom_out3, double* rho_out, void* scratch, void* stream) {
-  if (!vp || !xp || !fin || !fout || fin == fout || !speeds || !w || !v0 || !v2 || !xw ||
-      !mom_out3 || !rho_out || !scratch || !(dt > 0.0) ||
-      (bc != SLDG_BC_PERIODIC && bc != SLDG_BC_ABSORBING)) {
+  if (bad_step_args(vp, xp, fin, fout, speeds, bc, w, v0, v2, xw, scratch) || !mom_out3 ||
+      !rho_out || !(dt > 0.0)) {
     set_error("bad sldg_step_fused arguments");
     return SLDG_ERR_ARG;
   }
-  FusedGeom g = fused_geom(vp, xp, n_cols, ld);
-  if (!g.ok) {
-    set_error(g.why);
-    return SLDG_ERR_UNSUPPORTED;
-  }
-  if ((((unsigned long long)fin) & 15) != 0 || n_cols % 2 != 0) {
-    set_error("fused step: 16-byte aligned rows required");
-    return SLDG_ERR_UNSUPPORTED;
-  }
+  FusedGeom g;
+  int rc = check_geom(vp, xp, n_cols, ld, &g);
+  if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  unsigned char* sb = (unsigned char*)scratch;
-  long long* lm_ns = (long long*)sb;
-  size_t o1 = al256(sizeof(long long) * vp->dev.n_levels * n_cols);
-  double* lm_frac = (double*)(sb + o1);
-  size_t o2 = o1 + al256(sizeof(double) * vp->dev.n_levels * n_cols);
-  double* lm_mats = (double*)(sb + o2);
-  size_t o3 = o2 + al256(sizeof(double) * vp->dev.n_levels * 2 * vp->o * vp->o * n_cols);
-  double* mom_part = (double*)(sb + o3);
-  size_t o4 = o3 + al256(sizeof(double) * g.grid * 3);
-  double* rho_part = (double*)(sb + o4);
-  int rc = sldg_level_matrices(vp, speeds, n_cols, dt, (int64_t*)lm_ns, lm_frac, lm_mats, stream);
+  const FusedScratch s = fused_scratch(vp, g, n_cols, scratch);
+  rc = sldg_level_matrices(vp, speeds, n_cols, dt, (int64_t*)s.lm_ns, s.lm_frac, s.lm_mats, stream);
   if (rc) return rc;
-  FusedArgs fa{w, v0, v2, xw, mom_part, rho_part};
   long long grid = 0;
-  rc = SLDG_ERR_UNSUPPORTED;
-  switch (vp->o * 10 + xp->o) {
-#define CASE(A, B)                                                                          \
-  case A * 10 + B:                                                                          \
-    rc = launch_fused<A, B>(vp, xp, g, fin, fout, n_cols, speeds, bc, lm_ns, lm_mats, fa, st, \
-                            &grid);                                                         \
-    break;
-    CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(4, 2) CASE(4, 3)
-    CASE(4, 4)
-#undef CASE
-  }
+  rc = launch_step(vp, xp, g, fin, fout, n_cols, speeds, bc, s,
+                   FusedArgs{w, v0, v2, xw, s.mom_part, s.rho_part}, st, &grid);
   if (rc) return rc;
-  k_fold3<<<1, 96, 0, st>>>(mom_part, grid, mom_out3);
+  k_fold3<<<1, 96, 0, st>>>(s.mom_part, grid, mom_out3);
   SLDG_LAUNCH_CHECK("k_fold3");
-  k_fold_cols<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>(rho_part, grid, n_cols,
+  k_fold_cols<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>(s.rho_part, grid, n_cols,
                                                                       rho_out);
   SLDG_LAUNCH_CHECK("k_fold_cols");
+  return SLDG_OK;
+}
+
+int sldg_step_fused_deferred(const sldg_vplan* vp, const sldg_xplan* xp, const double* fin,
+                             double* fout, int64_t ld, int64_t n_cols, const double* speeds,
+                             int32_t bc, const double* w, const double* v0, const double* v2,
+                             const double* xw, void* scratch, void* stream) {
+  if (bad_step_args(vp, xp, fin, fout, speeds, bc, w, v0, v2, xw, scratch)) {
+    set_error("bad sldg_step_fused_deferred arguments");
+    return SLDG_ERR_ARG;
+  }
+  FusedGeom g;
+  int rc = check_geom(vp, xp, n_cols, ld, &g);
+  if (rc) return rc;
+  const FusedScratch s = fused_scratch(vp, g, n_cols, scratch);
+  long long grid = 0;
+  return launch_step(vp, xp, g, fin, fout, n_cols, speeds, bc, s,
+                     FusedArgs{w, v0, v2, xw, s.mom_part, s.rho_part}, (cudaStream_t)stream,
+                     &grid);
+}
+
+int sldg_field_chain(const sldg_vplan* vp, const sldg_xplan* xp, const sldg_poisson* P,
+                     int64_t n_cols, int64_t ld, double dt, const double* rho_in, double* rho,
+                     double* phi, double* e, double* diag2, double* mom_prev3, void* scratch,
+                     void* stream) {
+  if (!vp || !xp || !P || !phi || !e || !diag2 || !scratch || !(dt > 0.0) ||
+      (!rho_in && !rho) || n_cols != P->n_dofs) {
+    set_error("bad sldg_field_chain arguments");
+    return SLDG_ERR_ARG;
+  }
+  FusedGeom g;
+  int rc = check_geom(vp, xp, n_cols, ld, &g);
+  if (rc) return rc;
+  const FusedScratch s = fused_scratch(vp, g, n_cols, scratch);
+  long long grid = 0;
+  if (!rho_in) {   // partials of the previous sldg_step_fused_deferred
+    FusedKernel k = fused_kernel(vp, xp, g);
+    if (!k) {
+      set_error("fused step: no kernel for this degree / line group");
+      return SLDG_ERR_UNSUPPORTED;
+    }
+    rc = fused_grid(k, g, &grid);
+    if (rc) return rc;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (vp->o) {
+#define CASE(O)                                                                                \
+  case O:                                                                                      \
+    k_field_chain<O><<<1, 1024, 0, st>>>(                                                      \
+        rho_in, s.rho_part, s.mom_part, grid, mom_prev3, rho, P->xw, P->green, P->diff,        \
+        P->n_cells, P->p, P->length, P->h, P->work, phi, e, diag2, vp->basis, dt,              \
+        vp->dev.base_width, vp->dev.n_levels, s.lm_ns, s.lm_frac, s.lm_mats);                  \
+    break;
+    CASE(2) CASE(3) CASE(4)
+#undef CASE
+    default:
+      set_error("field chain: velocity degree 1..3");
+      return SLDG_ERR_UNSUPPORTED;
+  }
+  SLDG_LAUNCH_CHECK("k_field_chain");
   return SLDG_OK;
 }
 
