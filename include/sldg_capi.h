@@ -205,8 +205,10 @@ int sldg_step_fused(const sldg_vplan* vplan, const sldg_xplan* xplan, const doub
  * diag2 = [max|E|, field energy] (as sldg_field_diag) -> the v-sweep level
  * matrices for speeds = e into `scratch`; rho_in != NULL uses that rho instead.
  * sldg_step_fused_deferred is sldg_step_fused with those level matrices and with
- * the moment / rho partials left in `scratch` for the next sldg_field_chain.
- * Results are bitwise identical to the separate calls. */
+ * the moment / rho partials left in `scratch` for the next sldg_field_chain
+ * (mom_out3 != NULL folds the moments right away).  final_x = 1 is the last step
+ * of a run: f_out = X(V(f_in)), the state after the full step (no next leading
+ * half step, no rho).  Results are bitwise identical to the separate calls. */
 int sldg_field_chain(const sldg_vplan* vplan, const sldg_xplan* xplan, const sldg_poisson* p,
                      int64_t n_cols, int64_t ld, double dt, const double* rho_in, double* rho,
                      double* phi, double* e, double* diag2, double* mom_prev3, void* scratch,
@@ -214,7 +216,8 @@ int sldg_field_chain(const sldg_vplan* vplan, const sldg_xplan* xplan, const sld
 int sldg_step_fused_deferred(const sldg_vplan* vplan, const sldg_xplan* xplan,
                              const double* f_in, double* f_out, int64_t ld, int64_t n_cols,
                              const double* speeds, int32_t bc, const double* w, const double* v0,
-                             const double* v2, const double* xw, void* scratch, void* stream);
+                             const double* v2, const double* xw, int32_t final_x,
+                             double* mom_out3, void* scratch, void* stream);
 
 /* ---------------------------------------------------------------- misc */
 /* out[i*ld + j] = a[i] * b[j]: the separable initial condition sampled on the

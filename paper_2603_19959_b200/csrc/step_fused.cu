@@ -90,8 +90,10 @@ struct ItemTabs {
 };
 
 // NXC > 0: the row length (x cells) is a compile-time constant, so every shared
-// memory offset folds into the instruction (the headline configuration)
-template <int OV, int OX, int LG, int NXC>
+// memory offset folds into the instruction (the headline configuration).
+// FINAL: last step of a run -- X1's result is the state (stored to HBM), no X2
+// (a template flag: a runtime flag costs the steady-state kernel ~3%).
+template <int OV, int OX, int LG, int NXC, bool FINAL>
 __global__ void __launch_bounds__(384, 1)
 k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout,
              int n_cols_arg, int n_xc_arg, const double* __restrict__ speeds, int bc,
@@ -401,30 +403,41 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       __syncthreads();
       if (has_next && n_staged < 3) stage(n_staged, b ^ 1, it + 1);
       ++n_staged;
-      // ===================== X1 (trailing half step): stA -> stB, moments
-      if (xv) {
+      // ===================== X1 (trailing half step): stA -> stB (or HBM for the
+      // last step of a run), moments
+      auto x1 = [&](auto to_hbm) {
+        constexpr bool HBM = decltype(to_hbm)::value;
 #pragma unroll
         for (int t = 0; t < LG; ++t) {
           const int r = t * OV + iv;
           double y[OX];
           xapply(stA + r * rw, y);
           const double wr = mcur[r], wv0 = wr * mcur[R + r], wv2 = wr * mcur[2 * R + r];
-          double* o = stB + r * rw + cx * OX;
           double z = xws[cx * OX] * y[0];
 #pragma unroll
           for (int k = 1; k < OX; ++k) z = fma(xws[cx * OX + k], y[k], z);
+          if (HBM) {
+            double* o = fout + (r0 + r) * n_cols + cx * OX;
 #pragma unroll
-          for (int k = 0; k < OX; ++k) o[k] = y[k];
+            for (int k = 0; k < OX; ++k) o[k] = y[k];
+          } else {
+            double* o = stB + r * rw + cx * OX;
+#pragma unroll
+            for (int k = 0; k < OX; ++k) o[k] = y[k];
+          }
           m0 = fma(wr, z, m0);
           m1 = fma(wv0, z, m1);
           m2 = fma(wv2, z, m2);
         }
+      };
+      if (xv) {
+        x1(BoolC<FINAL>{});
       }
       __syncthreads();
       // ===================== X2 (next step's leading half): stB -> HBM, rho
       // No barrier after X2: the next V writes stA (last read in X1, before the
       // barrier above) and the ring slot it refills was last read in this V.
-      if (xv) {
+      if (xv && !FINAL) {
         double* dst = fout + (r0 + iv) * n_cols + cx * OX;
 #pragma unroll
         for (int t = 0; t < LG; ++t) {
@@ -550,25 +563,31 @@ using FusedKernel = void (*)(VPlanDev, XPlanDev, const double*, double*, int, in
                              int, const long long*, const double*, int, int, int, long long,
                              FusedArgs);
 
-template <int OV, int OX>
-static FusedKernel pick_kernel(int lg, long long n_xc) {
+template <int OV, int OX, bool FINAL>
+static FusedKernel pick_kernel_f(int lg, long long n_xc) {
   if (lg == OV) {
     if constexpr (OV == 3 && OX == 3) {
-      if (n_xc == 64) return k_step_fused<3, 3, 3, 64>;
+      if (n_xc == 64) return k_step_fused<3, 3, 3, 64, FINAL>;
     }
-    return k_step_fused<OV, OX, OV, 0>;
+    return k_step_fused<OV, OX, OV, 0, FINAL>;
   }
   if constexpr (OV % 2 == 0 && OV != 2) {
-    if (lg == 2) return k_step_fused<OV, OX, 2, 0>;
+    if (lg == 2) return k_step_fused<OV, OX, 2, 0, FINAL>;
   }
-  if (lg == 1) return k_step_fused<OV, OX, 1, 0>;
+  if (lg == 1) return k_step_fused<OV, OX, 1, 0, FINAL>;
   return nullptr;
 }
 
-static FusedKernel fused_kernel(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g) {
+template <int OV, int OX>
+static FusedKernel pick_kernel(int lg, long long n_xc, bool final_x) {
+  return final_x ? pick_kernel_f<OV, OX, true>(lg, n_xc) : pick_kernel_f<OV, OX, false>(lg, n_xc);
+}
+
+static FusedKernel fused_kernel(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
+                                bool final_x = false) {
   switch (vp->o * 10 + xp->o) {
 #define CASE(A, B) \
-  case A * 10 + B: return pick_kernel<A, B>(g.lg, xp->n_cells);
+  case A * 10 + B: return pick_kernel<A, B>(g.lg, xp->n_cells, final_x);
     CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(4, 2) CASE(4, 3)
     CASE(4, 4)
 #undef CASE
@@ -775,12 +794,13 @@ int check_geom(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_cols, int64
 
 int launch_step(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g, const double* fin,
                 double* fout, int64_t n_cols, const double* speeds, int32_t bc,
-                const FusedScratch& s, const FusedArgs& fa, cudaStream_t st, long long* grid) {
+                const FusedScratch& s, const FusedArgs& fa, int final_x, cudaStream_t st,
+                long long* grid) {
   if ((((unsigned long long)fin) & 15) != 0 || n_cols % 2 != 0) {
     set_error("fused step: 16-byte aligned rows required");
     return SLDG_ERR_UNSUPPORTED;
   }
-  FusedKernel k = fused_kernel(vp, xp, g);
+  FusedKernel k = fused_kernel(vp, xp, g, final_x != 0);
   if (!k) {
     set_error("fused step: no kernel for this degree / line group");
     return SLDG_ERR_UNSUPPORTED;
@@ -836,7 +856,7 @@ int sldg_step_fused(const sldg_vplan* vp, const sldg_xplan* xp, const double* fi
   if (rc) return rc;
   long long grid = 0;
   rc = launch_step(vp, xp, g, fin, fout, n_cols, speeds, bc, s,
-                   FusedArgs{w, v0, v2, xw, s.mom_part, s.rho_part}, st, &grid);
+                   FusedArgs{w, v0, v2, xw, s.mom_part, s.rho_part}, 0, st, &grid);
   if (rc) return rc;
   k_fold3<<<1, 96, 0, st>>>(s.mom_part, grid, mom_out3);
   SLDG_LAUNCH_CHECK("k_fold3");
@@ -849,8 +869,10 @@ int sldg_step_fused(const sldg_vplan* vp, const sldg_xplan* xp, const double* fi
 int sldg_step_fused_deferred(const sldg_vplan* vp, const sldg_xplan* xp, const double* fin,
                              double* fout, int64_t ld, int64_t n_cols, const double* speeds,
                              int32_t bc, const double* w, const double* v0, const double* v2,
-                             const double* xw, void* scratch, void* stream) {
-  if (bad_step_args(vp, xp, fin, fout, speeds, bc, w, v0, v2, xw, scratch)) {
+                             const double* xw, int32_t final_x, double* mom_out3, void* scratch,
+                             void* stream) {
+  if (bad_step_args(vp, xp, fin, fout, speeds, bc, w, v0, v2, xw, scratch) ||
+      (final_x != 0 && final_x != 1)) {
     set_error("bad sldg_step_fused_deferred arguments");
     return SLDG_ERR_ARG;
   }
@@ -858,10 +880,14 @@ int sldg_step_fused_deferred(const sldg_vplan* vp, const sldg_xplan* xp, const d
   int rc = check_geom(vp, xp, n_cols, ld, &g);
   if (rc) return rc;
   const FusedScratch s = fused_scratch(vp, g, n_cols, scratch);
+  cudaStream_t st = (cudaStream_t)stream;
   long long grid = 0;
-  return launch_step(vp, xp, g, fin, fout, n_cols, speeds, bc, s,
-                     FusedArgs{w, v0, v2, xw, s.mom_part, s.rho_part}, (cudaStream_t)stream,
-                     &grid);
+  rc = launch_step(vp, xp, g, fin, fout, n_cols, speeds, bc, s,
+                   FusedArgs{w, v0, v2, xw, s.mom_part, s.rho_part}, final_x, st, &grid);
+  if (rc || !mom_out3) return rc;
+  k_fold3<<<1, 96, 0, st>>>(s.mom_part, grid, mom_out3);
+  SLDG_LAUNCH_CHECK("k_fold3");
+  return SLDG_OK;
 }
 
 int sldg_field_chain(const sldg_vplan* vp, const sldg_xplan* xp, const sldg_poisson* P,
