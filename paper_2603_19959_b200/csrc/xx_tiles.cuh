@@ -69,8 +69,11 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     return cell * NLOC + (long long)tg * rpt * OV + iv;
   };
 
+  // a slot is full when warp 0's bulk copies have landed and (epilogues) warp 1's
+  // 32 lanes have arrived after their metadata cp.async copies
+  const bool need_meta = mom || rho;
   if (tid == 0) {
-    for (int k = 0; k < nring; ++k) mbar_init(&full[k], 1);
+    for (int k = 0; k < nring; ++k) mbar_init(&full[k], need_meta ? 33 : 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -78,7 +81,8 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
   const long long g0 = blockIdx.x, gs = gridDim.x;
   const long long my = g0 < n_groups ? (n_groups - g0 + gs - 1) / gs : 0;
   // issue group i (of this CTA) into slot i % nring: one bulk copy per row (warp 0),
-  // metadata by plain loads (threads of warp 1) into the slot's meta block
+  // metadata (w, v0, v2 of each row) by cp.async from warp 1 into the slot's meta
+  // block, completion signalled on the slot's barrier (no thread waits on it)
   auto issue = [&](long long i) {
     const int s = (int)(i % nring);
     const long long grp = g0 + i * gs;
@@ -93,18 +97,18 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
         bulk_g2s(ring + (long long)s * slot_dbl + (ti * rpt + u) * row_len, fin + row * ld,
                  (unsigned)(row_len * 8), &full[s]);
       }
-    } else if (tid < 64 && (mom || rho)) {
+    } else if (tid < 64 && need_meta) {
       for (int q = tid - 32; q < nt * rpt; q += 32) {
         const int ti = q / rpt, u = q - ti * rpt;
         const long long row = tile_row0(t_first + ti) + (long long)u * OV;
-        const double w = __ldg(epi.w + row);
         double* m = meta + (((long long)s * tpc + ti) * rpt + u) * 3;
-        m[0] = w;
+        cp_async8(m, epi.w + row);
         if (mom) {
-          m[1] = w * __ldg(epi.v0 + row);
-          m[2] = w * __ldg(epi.v2 + row);
+          cp_async8(m + 1, epi.v0 + row);
+          cp_async8(m + 2, epi.v2 + row);
         }
       }
+      cp_async_arrive(&full[s]);
     }
   };
   for (long long i = 0; i < min((long long)nring - 1, my); ++i) issue(i);
@@ -123,8 +127,7 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     const int g = g_next;
     g_next = speed_of(i + 1);                 // prefetched one group ahead
     const int s = (int)(i % nring);
-    mbar_wait(&full[s], (unsigned)((i / nring) & 1));
-    __syncthreads();                          // metadata of slot s visible
+    mbar_wait(&full[s], (unsigned)((i / nring) & 1));   // rows and metadata of slot s
     const long long t_first = (g0 + i * gs) * tpc;
     const long long tile = t_first + tt;
     const bool live = act && tile < n_tiles;
@@ -181,11 +184,12 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
 #pragma unroll
           for (int k = 0; k < OX; ++k) md[u * row_len + cx * OX + k] = y[k];
           if (mom) {
+            const double w = mt[u * 3], wv0 = w * mt[u * 3 + 1], wv2 = w * mt[u * 3 + 2];
 #pragma unroll
             for (int k = 0; k < OX; ++k) {
-              m0a[k] = fma(mt[u * 3], y[k], m0a[k]);
-              m1a[k] = fma(mt[u * 3 + 1], y[k], m1a[k]);
-              m2a[k] = fma(mt[u * 3 + 2], y[k], m2a[k]);
+              m0a[k] = fma(w, y[k], m0a[k]);
+              m1a[k] = fma(wv0, y[k], m1a[k]);
+              m2a[k] = fma(wv2, y[k], m2a[k]);
             }
           }
         }
@@ -198,14 +202,17 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
         double y[OX];
         xapply(src + u * row_len, y);
         double* dst = fout + (row0 + (long long)u * OV) * ld + cx * OX;
+        const double w = need_meta ? mt[u * 3] : 0.0;
+        const double wv0 = (mom && napply == 1) ? w * mt[u * 3 + 1] : 0.0;
+        const double wv2 = (mom && napply == 1) ? w * mt[u * 3 + 2] : 0.0;
 #pragma unroll
         for (int k = 0; k < OX; ++k) {
           dst[k] = y[k];
-          if (rho) rha[k] = fma(mt[u * 3], y[k], rha[k]);
+          if (rho) rha[k] = fma(w, y[k], rha[k]);
           if (mom && napply == 1) {
-            m0a[k] = fma(mt[u * 3], y[k], m0a[k]);
-            m1a[k] = fma(mt[u * 3 + 1], y[k], m1a[k]);
-            m2a[k] = fma(mt[u * 3 + 2], y[k], m2a[k]);
+            m0a[k] = fma(w, y[k], m0a[k]);
+            m1a[k] = fma(wv0, y[k], m1a[k]);
+            m2a[k] = fma(wv2, y[k], m2a[k]);
           }
         }
       }
