@@ -483,7 +483,10 @@ template <int OV, int OX>
 static int launch_xt_t(const sldg_xplan* X, const XTGeom& g, const double* fin, double* fout,
                        long long ld, int napply, bool mom, bool rho, const XEpi& epi,
                        cudaStream_t st) {
-  auto k = k_xx_tiles<OV, OX>;
+  auto k = k_xx_tiles<OV, OX, 0>;
+  if constexpr (OV == 3) {
+    if (g.rpt == 3) k = k_xx_tiles<OV, OX, 3>;
+  }
   SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
   k<<<(unsigned)g.grid_, g.threads, g.smem, st>>>(X->dev, fin, fout, ld, X->n_rows,
                                                   (int)X->n_cells, g.rpt, g.tpc, g.nring,

@@ -31,13 +31,16 @@ struct XTGeom {
 
 constexpr int kXTMaxTpc = 8;
 
-template <int OV, int OX>
+// RPT > 0: rows per tile fixed at compile time (row loops unrolled, tile -> row
+// arithmetic by constants); 0 = the geometry's value at run time.
+template <int OV, int OX, int RPT>
 __global__ void __launch_bounds__(512, 1)
 k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout, long long ld,
-           long long n_rows, int n_xc, int rpt, int tpc, int nring, int n_speeds, XEpi epi,
+           long long n_rows, int n_xc, int rpt_arg, int tpc, int nring, int n_speeds, XEpi epi,
            int napply, int mom, int rho) {
   constexpr int NL = OV * OV, NLOC = NL * OV;
   constexpr int XM = 2 * OX * OX;
+  const int rpt = RPT > 0 ? RPT : rpt_arg;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long full[4];
   const int row_len = n_xc * OX;
@@ -54,12 +57,13 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
   double* meta = mid + slot_dbl;             // [nring][tpc][rpt][3]: w, w*v0, w*v2
   double* xtab = meta + (long long)nring * tpc * rpt * 3;   // per speed: A | B
   int* xnsm = reinterpret_cast<int*>(xtab + (long long)n_speeds * XM);
-  unsigned char* xid = reinterpret_cast<unsigned char*>(xnsm + n_speeds);
-  for (int k = tid; k < n_speeds * XM; k += blockDim.x) xtab[k] = __ldg(X.mats + k);
-  for (int k = tid; k < n_speeds; k += blockDim.x) {
-    xnsm[k] = __ldg(X.nsm + k);
-    xid[k] = X.ident[k];
+  // a zero shift is stored as (A, B) = (I, 0) with no cell shift, so the update has
+  // no per-thread branch (1*u0 + 0*u1 + ... == u0)
+  for (int k = tid; k < n_speeds * XM; k += blockDim.x) {
+    const int g = k / XM, e = k - g * XM;
+    xtab[k] = X.ident[g] ? ((e < OX * OX && e % (OX + 1) == 0) ? 1.0 : 0.0) : __ldg(X.mats + k);
   }
+  for (int k = tid; k < n_speeds; k += blockDim.x) xnsm[k] = X.ident[k] ? 0 : __ldg(X.nsm + k);
 
   // tile id -> first row and row stride (rows u = 0..rpt-1 are row0 + u*OV)
   auto tile_row0 = [&](long long tile) -> long long {
@@ -132,12 +136,10 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     const long long tile = t_first + tt;
     const bool live = act && tile < n_tiles;
     double xa[OX * OX], xb[OX * OX];
-    bool ident = true;
     int ia = 0, ib = 0;
     long long row0 = 0;
     if (live) {
       row0 = tile_row0(tile);
-      ident = xid[g] != 0;
       const double* AB = xtab + (long long)g * XM;
 #pragma unroll
       for (int k = 0; k < OX * OX; ++k) {
@@ -146,15 +148,10 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
       }
       int a = cx - xnsm[g];   // nsm in [0, n_xc): the periodic source cell of cx
       if (a < 0) a += n_xc;
-      ia = (ident ? cx : a) * OX;
+      ia = a * OX;
       ib = (a == 0 ? n_xc - 1 : a - 1) * OX;
     }
     auto xapply = [&](const double* srow, double* y) {
-      if (ident) {
-#pragma unroll
-        for (int k = 0; k < OX; ++k) y[k] = srow[ia + k];
-        return;
-      }
       double ua[OX], ub[OX];
 #pragma unroll
       for (int j = 0; j < OX; ++j) {
@@ -178,6 +175,7 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     double* md = mid + tt * rpt * row_len;
     if (napply == 2) {
       if (live) {
+#pragma unroll(RPT > 0 ? RPT : 1)
         for (int u = 0; u < rpt; ++u) {
           double y[OX];
           xapply(src + u * row_len, y);
@@ -198,6 +196,7 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
       src = md;
     }
     if (live) {
+#pragma unroll(RPT > 0 ? RPT : 1)
       for (int u = 0; u < rpt; ++u) {
         double y[OX];
         xapply(src + u * row_len, y);
