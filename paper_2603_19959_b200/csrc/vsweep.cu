@@ -257,17 +257,17 @@ namespace sldg {
 
 // weighted write-back (vsweep.py:403-409): out = ((f_in + S_g1) + S_g2) + ...,
 // S_g = sum over the group's contributions in flat order of w (r - f_in).
+// Block x = one (target, local row), block y * blockDim + thread = column: the CSR
+// walk is uniform across the block and there is no per-thread 64-bit division.
 template <int NLOC>
 __global__ void k_writeback(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
                             long long ld, long long n_cols, const double* __restrict__ speeds,
                             const double* __restrict__ acc) {
-  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long per_t = (long long)NLOC * n_cols;
-  if (idx >= P.n_targets * per_t) return;
-  long long t = idx / per_t;
-  long long rem = idx - t * per_t;
-  int r = (int)(rem / n_cols);
-  long long c = rem - (long long)r * n_cols;
+  const long long tr = blockIdx.x;
+  const long long t = tr / NLOC;
+  const int r = (int)(tr - t * NLOC);
+  const long long c = (long long)blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= n_cols) return;
   long long row = P.t_row0[t] + r;
   double fv = fin[row * ld + c];
   if (__ldg(speeds + c) == 0.0) {
@@ -378,9 +378,9 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
     SLDG_LAUNCH_CHECK("k_sweep_generic");
   }
   if (p->n_targets > 0) {
-    long long n = p->n_targets * NLOC * n_cols;
-    k_writeback<NLOC><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p->dev, fin, fout, ld, n_cols,
-                                                                    speeds, acc);
+    const int threads = (int)std::min<long long>(256, (n_cols + 31) / 32 * 32);
+    const dim3 grid((unsigned)(p->n_targets * NLOC), (unsigned)((n_cols + threads - 1) / threads));
+    k_writeback<NLOC><<<grid, threads, 0, st>>>(p->dev, fin, fout, ld, n_cols, speeds, acc);
     SLDG_LAUNCH_CHECK("k_writeback");
   }
   return SLDG_OK;
