@@ -385,7 +385,10 @@ def test_sharded_world1_matches_simulation():
 FUSED_CASES = [dict(dim=3, n_base=8, levels=0, degree=2, n_x=32),
                dict(dim=3, n_base=16, levels=0, degree=1, n_x=16),
                dict(dim=3, n_base=6, levels=0, degree=3, n_x=24, bc="periodic"),
-               dict(dim=3, n_base=8, levels=0, degree=2, n_x=64, degree_x=1)]
+               dict(dim=3, n_base=8, levels=0, degree=2, n_x=64, degree_x=1),
+               # the compile-time 64-cell row of the headline shape (Q2, p_x = 2)
+               dict(dim=3, n_base=6, levels=0, degree=2, n_x=64),
+               dict(dim=3, n_base=5, levels=0, degree=2, n_x=64, bc="periodic")]
 
 
 @pytest.mark.parametrize("kw", FUSED_CASES)
@@ -406,6 +409,26 @@ def test_fused_step_matches_unfused_and_oracle(kw):
     for row, r in zip(ta, recs):
         assert abs(row[2] - r["m0"]) <= 1e-12 * abs(r["m0"])
         assert abs(row[0] - r["e_max"]) <= 1e-10 * recs[0]["e_max"]
+
+
+@pytest.mark.parametrize("kw", FUSED_CASES[:3] + FUSED_CASES[4:])
+def test_fused_last_step_mode_vs_unfused_and_oracle(kw):
+    """Simulation.step() on a fused-eligible plan: leading X + field chain + the fused
+    kernel's last-step mode (V + trailing X + moments) == the 3-pass step."""
+    a = sv.Simulation(sv.SimConfig(**kw, n_steps=2))
+    b = sv.Simulation(sv.SimConfig(**kw, n_steps=2))
+    b._fused_ok = False
+    ref = so.Sim(**kw)
+    for k in range(2):
+        ra, rb, rr = a.step(), b.step(), ref.step()
+        fa, fb = a.f.cpu().numpy(), b.f.cpu().numpy()
+        assert np.abs(fa - fb).max() <= 1e-13 * np.abs(fb).max()
+        assert np.abs(fa - ref.f).max() <= 1e-12 * np.abs(ref.f).max()
+        assert abs(ra.m0 - rb.m0) <= 1e-13 * abs(rb.m0)
+        assert abs(ra.m2 - rr["m2"]) <= 1e-12 * abs(rr["m2"])
+        if k == 0:   # same state, same rho: the field chain equals the separate kernels
+            assert ra.e_max == rb.e_max and ra.e_field == rb.e_field
+        assert abs(ra.e_max - rr["e_max"]) <= 1e-10 * abs(rr["e_max"])
 
 
 def test_run_uses_fused_step_and_matches_step_loop():
