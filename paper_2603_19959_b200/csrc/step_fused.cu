@@ -270,6 +270,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   long long nsv = 0;
   int cur_lev = -1;
   int base = 0;   // load index of the current item's first load
+  int waited = -1;   // highest load index this thread has waited for
 
   // V phase of one column: rows t*OV+i of the source cells sa / sb -> stA column c.
   // CHECKED: the source cells may lie outside the pencil (absorbing ends).
@@ -327,8 +328,11 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       if (streamable) {
         const int klo = base + max(s - 1, first) - first, khi = base + min(s + 1, last) - first;
         if (tid == 0) pump(klo + kFRing, i, n_staged >= 4);
-        for (int k = klo; k <= khi; ++k)
-          mbar_wait(&full[k & (kFRing - 1)], (unsigned)((k / kFRing) & 1));
+        // loads up to `waited` were waited for at earlier tiles (their slots are
+        // not refilled before every thread is past them): only the new ones
+        for (unsigned k = (unsigned)max(klo, waited + 1); k <= (unsigned)khi; ++k)
+          mbar_wait(&full[k & (kFRing - 1)], (k / kFRing) & 1u);
+        waited = max(waited, khi);
         if (colv) {
           auto slot = [&](int cell) { return ring + ((base + cell - first) & (kFRing - 1)) * tile + c; };
           if (speed == 0.0) {
@@ -648,23 +652,27 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
               DevBasis vb, double dt, double base_width, int n_levels,
               long long* __restrict__ lm_ns, double* __restrict__ lm_frac,
               double* __restrict__ lm_mats) {
-  constexpr int CH = 64;   // columns per fold chunk
+  constexpr int CH = 80;   // columns per fold chunk
   __shared__ double red[1024], red2[1024];
   __shared__ double fsm[32 * (CH + 1)];
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, nw = blockDim.x >> 5;
   const int o = p + 1;
   const long long n_dofs = n_cells * o, n_nodes = n_cells * p;
+  const int nd = (int)n_dofs, np = (int)n_parts;
   const double* r = rho_in;
   if (!r) {
     // fold the previous fused step's partials in k_fold_cols' order (lane l sums
     // parts l, l+32, ...; then the xor butterfly), with coalesced loads: thread
     // (l, column) forms lane l's sum, a warp per column does the butterfly
-    for (long long c0 = 0; c0 < n_dofs; c0 += CH) {
-      const int nc = (int)min((long long)CH, n_dofs - c0);
+    for (int c0 = 0; c0 < nd; c0 += CH) {
+      const int nc = min(CH, nd - c0);
       for (int idx = tid; idx < 32 * nc; idx += blockDim.x) {
         const int l = idx / nc, cc = idx - l * nc;
+        const double* q = rho_part + (size_t)l * nd + c0 + cc;
+        const size_t stride = (size_t)32 * nd;
         double s = 0.0;
-        for (long long k = l; k < n_parts; k += 32) s += rho_part[k * n_dofs + c0 + cc];
+#pragma unroll 4
+        for (int k = l; k < np; k += 32, q += stride) s += __ldg(q);
         fsm[l * (CH + 1) + cc] = s;
       }
       __syncthreads();
@@ -711,12 +719,17 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
       v = __dmul_rn(pxw[k], __dsub_rn(r[k], rbar));
     }
     b[node] = v;
+    if (n_nodes <= 32 * (CH + 1)) fsm[node] = v;   // b staged in shared memory for the GEMV
   }
   __syncthreads();
   // phi = G b (k_gemv: warp per row)
-  for (long long row = wp; row < n_nodes; row += nw) {
+  const int nn = (int)n_nodes;
+  const double* bsrc = nn <= 32 * (CH + 1) ? fsm : b;
+  for (int row = wp; row < nn; row += nw) {
     double t = 0.0;
-    for (long long k = lane; k < n_nodes; k += 32) t = fma(__ldg(green + row * n_nodes + k), b[k], t);
+    const double* g = green + (size_t)row * nn;
+#pragma unroll 4
+    for (int k = lane; k < nn; k += 32) t = fma(__ldg(g + k), bsrc[k], t);
 #pragma unroll
     for (int of = 16; of > 0; of >>= 1) t += __shfl_xor_sync(0xffffffffu, t, of);
     if (lane == 0) phi[row] = t;
