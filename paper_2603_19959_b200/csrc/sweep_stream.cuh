@@ -21,6 +21,8 @@
 // Landau shifts; checked per tile): cell s then needs cells s-1, s, s+1.
 #pragma once
 
+#include <type_traits>
+
 #include "tma_util.cuh"
 
 namespace sldg {
@@ -136,13 +138,18 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     for (int k = 0; k < min(3, n_load); ++k) issue(k);
   }
   // per-line row offsets (compile-time for direction 0)
+  int waited = -1;
   for (int s = 0; s < n; ++s) {
     // prefetch list position of virtual cell s+2
     const int kn = s + 2 - v0;
     if (tid < 32 && kn < n_load && kn >= 3) issue(kn);
-    // wait for virtual cells s-1 .. s+1 that exist in the list
+    // wait for virtual cells s-1 .. s+1 that exist in the list; the ones below
+    // `waited` were waited for at an earlier cell (their slots are refilled only
+    // after every thread is past them)
     const int klo = max(s - 1 - v0, 0), khi = min(s + 1 - v0, n_load - 1);
-    for (int k = klo; k <= khi; ++k) mbar_wait(&full[k % kStreamRing], (unsigned)((k / kStreamRing) & 1));
+    for (unsigned k = (unsigned)max(klo, waited + 1); k <= (unsigned)khi; ++k)
+      mbar_wait(&full[k % kStreamRing], (k / kStreamRing) & 1u);
+    waited = max(waited, khi);
     if (colv) {
       const long long e = off + s;
       const int slot = P.e_slot[e];
@@ -154,27 +161,35 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
 #pragma unroll 3
         for (int r = 0; r < NLOC; ++r) dst[r * dstride] = me[r * rstride];
       } else {
-        // sources: virtual cells s - ns (same) and s - ns - 1 (neighbour)
+        // sources: virtual cells s - ns (same) and s - ns - 1 (neighbour); both in
+        // the pencil unless an absorbing end cuts one off (first / last cell only)
         const int va_cell = s - (int)ns, vb_cell = s - (int)ns - 1;
-        const bool va = per || (va_cell >= 0 && va_cell < n);
-        const bool vb = per || (vb_cell >= 0 && vb_cell < n);
-        const double* sa = sm + ((va ? va_cell : s) - v0) % kStreamRing * cell_dbl + tid;
-        const double* sb = sm + ((vb ? vb_cell : s) - v0) % kStreamRing * cell_dbl + tid;
+        auto apply = [&](bool va, bool vb, auto checked) {
+          constexpr bool CK = decltype(checked)::value;
+          const double* sa = sm + (unsigned)((va ? va_cell : s) - v0) % kStreamRing * cell_dbl + tid;
+          const double* sb = sm + (unsigned)((vb ? vb_cell : s) - v0) % kStreamRing * cell_dbl + tid;
 #pragma unroll
-        for (int t = 0; t < NL; ++t) {
-          double ua[O], ub[O], y[O];
+          for (int t = 0; t < NL; ++t) {
+            double ua[O], ub[O], y[O];
 #pragma unroll
-          for (int i = 0; i < O; ++i) {
-            const int r = (DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i;
-            ua[i] = va ? sa[r * rstride] : 0.0;
-            ub[i] = vb ? sb[r * rstride] : 0.0;
+            for (int i = 0; i < O; ++i) {
+              const int r = (DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i;
+              ua[i] = (!CK || va) ? sa[r * rstride] : 0.0;
+              ub[i] = (!CK || vb) ? sb[r * rstride] : 0.0;
+            }
+            two_cell<O>(A, B, ua, ub, !CK || va, !CK || vb, y);
+#pragma unroll
+            for (int i = 0; i < O; ++i) {
+              const int r = (DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i;
+              dst[(long long)r * dstride] = y[i];
+            }
           }
-          two_cell<O>(A, B, ua, ub, va, vb, y);
-#pragma unroll
-          for (int i = 0; i < O; ++i) {
-            const int r = (DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i;
-            dst[(long long)r * dstride] = y[i];
-          }
+        };
+        if (per || (va_cell >= 0 && va_cell < n && vb_cell >= 0 && vb_cell < n)) {
+          apply(true, true, std::integral_constant<bool, false>{});
+        } else {
+          apply(va_cell >= 0 && va_cell < n, vb_cell >= 0 && vb_cell < n,
+                std::integral_constant<bool, true>{});
         }
       }
     }
