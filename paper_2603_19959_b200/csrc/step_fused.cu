@@ -150,20 +150,9 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   }
   __syncthreads();
 
-  // ---- V-phase state: thread = column; a level is streamable when every moving
-  // column's integer shift is -1 or 0 (sources in cells s-1, s, s+1)
+  const bool per = (bc == SLDG_BC_PERIODIC);
   const bool colv = tid < n_cols;
   const int c = tid;
-  const double speed = colv ? __ldg(speeds + c) : 0.0;
-  if (colv && speed != 0.0) {
-    for (int L = 0; L < P.n_levels; ++L) {
-      const long long v = lm_ns[(long long)L * n_cols + c];
-      const int nsi = (int)max(min(v, (long long)(1 << 29)), -(long long)(1 << 29));
-      atomicMin(&s_nsmin[L], nsi);
-      atomicMax(&s_nsmax[L], nsi);
-    }
-  }
-  const bool per = (bc == SLDG_BC_PERIODIC);
 
   // ---- X-phase state: thread = (iv, x cell)
   const bool xv = tid < OV * n_xc;
@@ -214,6 +203,23 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
 
   // item 0 tables, synchronously
   for (int st = 0; st < 3; ++st) stage_sync(st, 0, it_first);
+
+  // Everything above depends only on the plans and the state, so under
+  // programmatic dependent launch it overlaps the preceding field chain; E and
+  // the level matrices it writes are read only from here on.
+  grid_dep_wait();
+  // ---- V-phase state: thread = column; a level is streamable when every moving
+  // column's integer shift is -1 or 0 (sources in cells s-1, s, s+1)
+  const double speed = colv ? __ldg(speeds + c) : 0.0;
+  if (colv && speed != 0.0) {
+    for (int L = 0; L < P.n_levels; ++L) {
+      const long long v = lm_ns[(long long)L * n_cols + c];
+      const int nsi = (int)max(min(v, (long long)(1 << 29)), -(long long)(1 << 29));
+      atomicMin(&s_nsmin[L], nsi);
+      atomicMax(&s_nsmax[L], nsi);
+    }
+  }
+  __syncthreads();
 
   // ---- ring of cell tiles: one load sequence across the CTA's items.  Item i's
   // loads are the cells first..last of its segment (sb-1..se, wrapped when
@@ -466,7 +472,8 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       for (int st = max(n_staged, 0); st < 3; ++st) stage_sync(st, b ^ 1, it + 1);
     }
   }
-  __syncthreads();   // stB (read by X2) is reused by the reduction below
+  grid_dep_launch();   // the next field chain may be scheduled (it waits for our end)
+  __syncthreads();     // stB (read by X2) is reused by the reduction below
 
   // ---- CTA partials: rho per column (over i_v in order), moments contracted with xw
   double* red = stA;   // reuse: OV x n_cols, then 3 x blockDim
@@ -610,6 +617,24 @@ static int fused_grid(FusedKernel k, const FusedGeom& g, long long* grid) {
 
 static size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
+// launch with programmatic stream serialization: the kernel may start while the
+// previous kernel in the stream finishes; it orders itself with grid_dep_wait()
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
 // scratch of the fused step: level matrices, then the CTA partials
 struct FusedScratch {
   long long* lm_ns;
@@ -659,6 +684,10 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
   const int o = p + 1;
   const long long n_dofs = n_cells * o, n_nodes = n_cells * p;
   const int nd = (int)n_dofs, np = (int)n_parts;
+  // PDL: wait for the preceding fused step (its partials and state are complete),
+  // then let the next fused step start its E-independent prologue alongside us
+  grid_dep_wait();
+  grid_dep_launch();
   const double* r = rho_in;
   if (!r) {
     // fold the previous fused step's partials in k_fold_cols' order (lane l sums
@@ -820,9 +849,10 @@ int launch_step(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g, 
   }
   int rc = fused_grid(k, g, grid);
   if (rc) return rc;
-  k<<<(unsigned)*grid, g.threads, g.smem, st>>>(vp->dev, xp->dev, fin, fout, (int)n_cols,
-                                                (int)xp->n_cells, speeds, bc, s.lm_ns, s.lm_mats,
-                                                g.rw, (int)xp->n_speeds, g.nmax, g.n_tiles, fa);
+  SLDG_CUDA_TRY(launch_pdl(k, dim3((unsigned)*grid), dim3(g.threads), g.smem, st, vp->dev,
+                           xp->dev, fin, fout, (int)n_cols, (int)xp->n_cells, speeds, (int)bc,
+                           (const long long*)s.lm_ns, (const double*)s.lm_mats, g.rw,
+                           (int)xp->n_speeds, g.nmax, g.n_tiles, fa));
   SLDG_LAUNCH_CHECK("k_step_fused");
   return SLDG_OK;
 }
@@ -930,10 +960,12 @@ int sldg_field_chain(const sldg_vplan* vp, const sldg_xplan* xp, const sldg_pois
   switch (vp->o) {
 #define CASE(O)                                                                                \
   case O:                                                                                      \
-    k_field_chain<O><<<1, 1024, 0, st>>>(                                                      \
-        rho_in, s.rho_part, s.mom_part, grid, mom_prev3, rho, P->xw, P->green, P->diff,        \
-        P->n_cells, P->p, P->length, P->h, P->work, phi, e, diag2, vp->basis, dt,              \
-        vp->dev.base_width, vp->dev.n_levels, s.lm_ns, s.lm_frac, s.lm_mats);                  \
+    SLDG_CUDA_TRY(launch_pdl(k_field_chain<O>, dim3(1), dim3(1024), 0, st, rho_in,           \
+                             (const double*)s.rho_part, (const double*)s.mom_part, grid,       \
+                             mom_prev3, rho, (const double*)P->xw, (const double*)P->green,    \
+                             (const double*)P->diff, P->n_cells, P->p, P->length, P->h,        \
+                             P->work, phi, e, diag2, vp->basis, dt, vp->dev.base_width,        \
+                             vp->dev.n_levels, s.lm_ns, s.lm_frac, s.lm_mats));                \
     break;
     CASE(2) CASE(3) CASE(4)
 #undef CASE
