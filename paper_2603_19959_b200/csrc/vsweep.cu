@@ -257,37 +257,56 @@ namespace sldg {
 
 // weighted write-back (vsweep.py:403-409): out = ((f_in + S_g1) + S_g2) + ...,
 // S_g = sum over the group's contributions in flat order of w (r - f_in).
-// Block x = one (target, local row), block y * blockDim + thread = column: the CSR
-// walk is uniform across the block and there is no per-thread 64-bit division.
+// Block x = one target cell (its contribution list staged in shared memory once),
+// block y * blockDim + thread = column, each thread walks the cell's NLOC rows.
+constexpr int kWbMaxC = 32;   // contributions per target staged in shared memory
+
 template <int NLOC>
-__global__ void k_writeback(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
-                            long long ld, long long n_cols, const double* __restrict__ speeds,
-                            const double* __restrict__ acc) {
-  const long long tr = blockIdx.x;
-  const long long t = tr / NLOC;
-  const int r = (int)(tr - t * NLOC);
+__global__ void __launch_bounds__(256)
+k_writeback(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout, long long ld,
+            long long n_cols, const double* __restrict__ speeds, const double* __restrict__ acc) {
+  __shared__ const double* s_src[kWbMaxC];   // acc row 0 of each contribution's slot
+  __shared__ int s_grp[kWbMaxC];
+  __shared__ double s_w[kWbMaxC];
+  const long long t = blockIdx.x;
+  const long long k0 = P.t_off[t];
+  const int nk = (int)(P.t_off[t + 1] - k0);
+  const int ns = min(nk, kWbMaxC);
+  for (int k = threadIdx.x; k < ns; k += blockDim.x) {
+    s_src[k] = acc + (long long)P.c_slot[k0 + k] * NLOC * n_cols;
+    s_grp[k] = P.c_group[k0 + k];
+    s_w[k] = P.c_weight[k0 + k];
+  }
+  __syncthreads();
   const long long c = (long long)blockIdx.y * blockDim.x + threadIdx.x;
   if (c >= n_cols) return;
-  long long row = P.t_row0[t] + r;
-  double fv = fin[row * ld + c];
-  if (__ldg(speeds + c) == 0.0) {
-    fout[row * ld + c] = fv;
-    return;
-  }
-  long long k0 = P.t_off[t], k1 = P.t_off[t + 1];
-  double o = fv, s = 0.0;
-  int g = P.c_group[k0];
-  for (long long k = k0; k < k1; ++k) {
-    int gk = P.c_group[k];
-    if (gk != g) {
-      o = __dadd_rn(o, s);
-      s = 0.0;
-      g = gk;
+  const bool moving = __ldg(speeds + c) != 0.0;
+  const long long row0 = P.t_row0[t];
+#pragma unroll 3
+  for (int r = 0; r < NLOC; ++r) {
+    const long long at = (row0 + r) * ld + c;
+    const double fv = fin[at];
+    if (!moving) {   // exact-zero speed: untouched bits
+      fout[at] = fv;
+      continue;
     }
-    double rv = acc[((long long)P.c_slot[k] * NLOC + r) * n_cols + c];
-    s = __dadd_rn(s, __dmul_rn(P.c_weight[k], __dsub_rn(rv, fv)));
+    double o = fv, s = 0.0;
+    int g = s_grp[0];
+    for (int k = 0; k < nk; ++k) {
+      const bool sh = k < kWbMaxC;
+      const int gk = sh ? s_grp[k] : P.c_group[k0 + k];
+      if (gk != g) {
+        o = __dadd_rn(o, s);
+        s = 0.0;
+        g = gk;
+      }
+      const double* src = sh ? s_src[k] : acc + (long long)P.c_slot[k0 + k] * NLOC * n_cols;
+      const double wk = sh ? s_w[k] : P.c_weight[k0 + k];
+      const double rv = src[(long long)r * n_cols + c];
+      s = __dadd_rn(s, __dmul_rn(wk, __dsub_rn(rv, fv)));
+    }
+    fout[at] = __dadd_rn(o, s);
   }
-  fout[row * ld + c] = __dadd_rn(o, s);
 }
 
 // ---------------------------------------------------------------------------
@@ -379,7 +398,7 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
   }
   if (p->n_targets > 0) {
     const int threads = (int)std::min<long long>(256, (n_cols + 31) / 32 * 32);
-    const dim3 grid((unsigned)(p->n_targets * NLOC), (unsigned)((n_cols + threads - 1) / threads));
+    const dim3 grid((unsigned)p->n_targets, (unsigned)((n_cols + threads - 1) / threads));
     k_writeback<NLOC><<<grid, threads, 0, st>>>(p->dev, fin, fout, ld, n_cols, speeds, acc);
     SLDG_LAUNCH_CHECK("k_writeback");
   }
