@@ -103,6 +103,29 @@ int sldg_level_matrices(const sldg_vplan* plan, const double* speeds, int64_t n_
 int sldg_overlap_pairs(const SldgBasis* basis, const double* fracs, int64_t n, double* A,
                        double* B, void* stream);
 
+/* Pure pencil-level functions of the reference (all device pointers):
+ * apply_update (sldg1d.py:124-136): values/out (n_batch, n_cells, o) row-major,
+ *   out_i = A v_{i-n_shift} + B v_{i-n_shift-1} (periodic wrap / absorbing zero fill);
+ * projection_oracle (sldg1d.py:139-178): brute-force projection of the translated
+ *   piecewise polynomial, Gauss rule gq/gw (nq points, e.g. 50) on every overlap;
+ * generalized_overlap (vsweep.py:98-122): o x o block M^-1 (2/w_d) int_vl^vr l_i l_j
+ *   for the overlap [vl, vr] (vl < vr) of a foot with a source cell;
+ * weighted_writeback (vsweep.py:249-272): flat contributions grouped per element in
+ *   increasing flat order (csr_off[n+1], csr_idx): copies (w == 1) in order, then
+ *   out += sum of w (v - f_in), as numpy's assignment + bincount. */
+int sldg_apply_update(const double* values, int64_t n_batch, int64_t n_cells, int32_t o,
+                      int64_t n_shift, const double* A, const double* B, int32_t bc, double* out,
+                      void* stream);
+int sldg_projection_oracle(const SldgBasis* basis, const double* values, int64_t n_cells,
+                           double displacement, double width, int32_t bc, const double* gq,
+                           const double* gw, int32_t nq, double* out, void* stream);
+int sldg_generalized_overlap(const SldgBasis* basis, double vl, double vr, double dest_lo,
+                             double dest_width, double src_lo, double src_width,
+                             double displacement, double* matrix, void* stream);
+int sldg_weighted_writeback(const double* f_in, int64_t n, const int64_t* csr_off,
+                            const int64_t* csr_idx, const double* weights, const double* values,
+                            double* out, void* stream);
+
 /* ---------------------------------------------------------------- x side */
 typedef struct sldg_xplan sldg_xplan;
 

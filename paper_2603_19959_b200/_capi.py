@@ -86,6 +86,16 @@ _SIGS = {
                              C.c_int64, C.c_void_p]),
     "sldg_overlap_pairs": (C.c_int, [C.POINTER(SldgBasis), C.c_void_p, C.c_int64, C.c_void_p,
                                      C.c_void_p, C.c_void_p]),
+    "sldg_apply_update": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int64,
+                                    C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "sldg_projection_oracle": (C.c_int, [C.POINTER(SldgBasis), C.c_void_p, C.c_int64, C.c_double,
+                                         C.c_double, C.c_int32, C.c_void_p, C.c_void_p,
+                                         C.c_int32, C.c_void_p, C.c_void_p]),
+    "sldg_generalized_overlap": (C.c_int, [C.POINTER(SldgBasis), C.c_double, C.c_double,
+                                           C.c_double, C.c_double, C.c_double, C.c_double,
+                                           C.c_double, C.c_void_p, C.c_void_p]),
+    "sldg_weighted_writeback": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sldg_vplan_create": (C.c_int, [C.POINTER(SldgVPlanDesc), C.POINTER(C.c_void_p)]),
     "sldg_vplan_destroy": (C.c_int, [C.c_void_p]),
     "sldg_vplan_scratch_bytes": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_size_t)]),

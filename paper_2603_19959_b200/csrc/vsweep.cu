@@ -405,11 +405,53 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
   return SLDG_OK;
 }
 
+// generalized_overlap (vsweep.py:98-122) for one (destination, source) pair: the
+// slow path's own block routine, one thread
+template <int O>
+__global__ void k_generalized_overlap(DevBasis b, double vl, double vr, double dlo, double dw,
+                                      double slo, double sw, double de, double* __restrict__ M) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double m[O * O];
+  general_block<O>(b, vl, vr, dlo, dw, slo, sw, de, m);
+#pragma unroll
+  for (int k = 0; k < O * O; ++k) M[k] = m[k];
+}
+
 }  // namespace sldg
 
 using namespace sldg;
 
 extern "C" {
+
+int sldg_generalized_overlap(const SldgBasis* basis, double vl, double vr, double dest_lo,
+                             double dest_width, double src_lo, double src_width,
+                             double displacement, double* matrix, void* stream) {
+  DevBasis b;
+  std::string err;
+  if (!basis || !make_dev_basis(*basis, &b, &err)) {
+    set_error(basis ? err : "null basis");
+    return SLDG_ERR_ARG;
+  }
+  if (!matrix || !(dest_width > 0.0) || !(src_width > 0.0) || !(vr > vl)) {
+    set_error("bad generalized_overlap arguments");
+    return SLDG_ERR_ARG;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (b.o) {
+#define CASE(O)                                                                             \
+  case O:                                                                                   \
+    k_generalized_overlap<O><<<1, 32, 0, st>>>(b, vl, vr, dest_lo, dest_width, src_lo,     \
+                                               src_width, displacement, matrix);            \
+    break;
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
+#undef CASE
+    default:
+      set_error("generalized_overlap: degree 1..5");
+      return SLDG_ERR_UNSUPPORTED;
+  }
+  SLDG_LAUNCH_CHECK("k_generalized_overlap");
+  return SLDG_OK;
+}
 
 int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
   if (!d || !out) {

@@ -3,7 +3,8 @@
 `decompose_shift` is the scalar split every kernel restates on the device
 (bit-identical, csrc/sldg_common.cuh split_shift); `overlap_pair` evaluates
 the A/B projection blocks ON THE DEVICE through sldg_overlap_pairs -- the same
-code the sweep kernels run per column and level.
+code the sweep kernels run per column and level.  `apply_update` and
+`projection_oracle` (sldg1d.py:124-178) run as kernels too (csrc/pencil_ops.cu).
 """
 from __future__ import annotations
 
@@ -78,3 +79,61 @@ def overlap_pair(basis, frac: float) -> OverlapPair:
         raise ValueError(f"fractional shift must lie in [0, 1), got {frac}")
     A, B = overlap_pairs_device(basis, [frac])
     return OverlapPair(A[0], B[0], float(frac))
+
+
+def apply_update(values, decomp: ShiftDecomposition, pair: OverlapPair, bc: str = PERIODIC):
+    """One SLDG step on a uniform pencil, on the device (apply_update, sldg1d.py:124-136).
+
+    `values` has shape (..., n_cells, p+1) (numpy, or a CUDA float64 tensor, which
+    is then also what is returned); destination cell i draws from source cells
+    i - n_shift and i - n_shift - 1 (periodic wrap, absorbing zero fill).
+    """
+    import torch
+
+    from . import _capi
+    from ._device import current_stream, device, is_device_tensor
+    check_bc(bc)
+    on_dev = is_device_tensor(values)
+    v = values if on_dev else np.asarray(values, dtype=float)
+    if v.ndim < 2:
+        raise ValueError("expected pencil values of shape (..., n_cells, p+1)")
+    n, o = int(v.shape[-2]), int(v.shape[-1])
+    A = np.ascontiguousarray(pair.same, dtype=np.float64)
+    B = np.ascontiguousarray(pair.neighbor, dtype=np.float64)
+    if A.shape != (o, o) or B.shape != (o, o):
+        raise ValueError(f"overlap pair shaped {A.shape}, values have {o} nodes per cell")
+    dev = device()
+    vd = (v.to(torch.float64).contiguous() if on_dev
+          else torch.from_numpy(np.ascontiguousarray(v)).to(dev))
+    out = torch.empty_like(vd)
+    Ad, Bd = torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev)
+    n_batch = vd.numel() // (n * o) if n * o else 0
+    _capi.check(_capi.lib().sldg_apply_update(vd.data_ptr(), n_batch, n, o, int(decomp.n_shift),
+                                              Ad.data_ptr(), Bd.data_ptr(), _capi.BC_CODE[bc],
+                                              out.data_ptr(), current_stream()), ValueError)
+    return out if on_dev else out.cpu().numpy()
+
+
+def projection_oracle(values, displacement: float, width: float, basis, bc: str = PERIODIC):
+    """Brute-force projection of the exactly translated pencil (sldg1d.py:139-178), on
+    the device: 50-point Gauss quadrature over every overlap of the foot of cell
+    i = [i w, (i+1) w) - displacement with a source cell (and its periodic images)."""
+    import torch
+
+    from . import _capi
+    from ._device import current_stream, device
+    check_bc(bc)
+    v = np.ascontiguousarray(np.asarray(values, dtype=float))
+    if v.ndim != 2 or v.shape[1] != basis.n_nodes:
+        raise ValueError(f"expected values of shape (n_cells, {basis.n_nodes})")
+    gq, gw = np.polynomial.legendre.leggauss(50)
+    dev = device()
+    vd = torch.from_numpy(v).to(dev)
+    gqd, gwd = torch.from_numpy(gq).to(dev), torch.from_numpy(gw).to(dev)
+    out = torch.empty_like(vd)
+    ba = _capi.BasisArrays(basis)
+    _capi.check(_capi.lib().sldg_projection_oracle(
+        ba.struct, vd.data_ptr(), v.shape[0], float(displacement), float(width),
+        _capi.BC_CODE[bc], gqd.data_ptr(), gwd.data_ptr(), gq.size, out.data_ptr(),
+        current_stream()), ValueError)
+    return out.cpu().numpy()

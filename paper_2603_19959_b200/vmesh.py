@@ -151,3 +151,14 @@ def build_mesh(dim: int, n_base: int, max_level: int, radius: float, marker=None
 def ip_count(mesh: VelocityMesh, degree: int) -> int:
     """Total integration points (vmesh.py:171-173)."""
     return mesh.n_cells * (degree + 1) ** mesh.dim
+
+
+def dump_mesh(mesh: VelocityMesh, path) -> None:
+    """Cell list as CSV: id, level, lower corner, widths, %.17e (vmesh.py:176-187)."""
+    names = ["cell", "level"] + [f"lo_{d}" for d in range(mesh.dim)] + \
+        [f"h_{d}" for d in range(mesh.dim)]
+    with open(path, "w", newline="\n") as fh:
+        fh.write(",".join(names) + "\n")
+        for i in range(mesh.n_cells):
+            vals = [f"{v:.17e}" for v in (*mesh.lo[i], *mesh.width[i])]
+            fh.write(",".join([str(i), str(int(mesh.levels[i]))] + vals) + "\n")

@@ -183,6 +183,115 @@ def build_sweep_plan(mesh: VelocityMesh, pset: PencilSet, perm: TensorPermutatio
                      int(mesh.levels.max()) + 1, n_dofs, groups, mesh.dim, mesh.n_cells, arrays)
 
 
+@dataclass(frozen=True)
+class GeneralizedOverlap:
+    """Projection block of one source cell onto one destination cell (vsweep.py:64-74):
+    `matrix` includes M^-1; [lo, hi] is the foot/source overlap in foot coordinates."""
+
+    matrix: np.ndarray
+    lo: float
+    hi: float
+
+
+def generalized_overlap(basis: DGBasis, dest_lo: float, dest_width: float, src_lo: float,
+                        src_width: float, displacement: float) -> GeneralizedOverlap:
+    """Cross-size projection block (vsweep.py:98-122), evaluated on the device by the slow
+    path's own block routine (csrc/vsweep.cu general_block)."""
+    import torch
+
+    from ._device import current_stream, device
+    if dest_width <= 0 or src_width <= 0:
+        raise ValueError("cell widths must be positive")
+    o = basis.n_nodes
+    foot_lo = dest_lo - displacement
+    vl = max(foot_lo, src_lo)
+    vr = min(foot_lo + dest_width, src_lo + src_width)
+    if vr <= vl:
+        return GeneralizedOverlap(np.zeros((o, o)), vl, vl)
+    m = torch.empty((o, o), dtype=torch.float64, device=device())
+    ba = _capi.BasisArrays(basis)
+    _capi.check(_capi.lib().sldg_generalized_overlap(
+        ba.struct, float(vl), float(vr), float(dest_lo), float(dest_width), float(src_lo),
+        float(src_width), float(displacement), m.data_ptr(), current_stream()), ValueError)
+    return GeneralizedOverlap(m.cpu().numpy(), vl, vr)
+
+
+def weighted_writeback(f_in, gather, weights, values):
+    """f_out = f_in + sum over contributions of w (value - f_in), a copy where w == 1
+    (vsweep.py:249-272), on the device with numpy's order: copies in flat order, then
+    the weighted deltas summed per element in flat order."""
+    import torch
+
+    from ._device import current_stream, device
+    f = np.ascontiguousarray(np.asarray(f_in, dtype=float))
+    g = np.asarray(gather, dtype=np.int64).ravel()
+    w = np.ascontiguousarray(np.asarray(weights, dtype=float).ravel())
+    v = np.ascontiguousarray(np.asarray(values, dtype=float).ravel())
+    if not (g.size == w.size == v.size):
+        raise ValueError("gather, weights and values must be aligned")
+    counts = np.bincount(g, minlength=f.size)
+    if (counts == 0).any():
+        missing = int(np.nonzero(counts == 0)[0][0])
+        raise SweepError(f"element {missing} has zero total write-back weight")
+    order = np.argsort(g, kind="stable").astype(np.int64)   # per element, flat order
+    off = np.concatenate(([0], np.cumsum(counts))).astype(np.int64)
+    dev = device()
+    fd = torch.from_numpy(f.ravel().copy()).to(dev)
+    out = torch.empty_like(fd)
+    args = [torch.from_numpy(a).to(dev) for a in (off, order, w, v)]
+    _capi.check(_capi.lib().sldg_weighted_writeback(
+        fd.data_ptr(), f.size, args[0].data_ptr(), args[1].data_ptr(), args[2].data_ptr(),
+        args[3].data_ptr(), out.data_ptr(), current_stream()), SweepError)
+    return out.cpu().numpy().reshape(f.shape)
+
+
+def sweep_pencil(values, lowers, widths, levels, conforming, speed, dt, lm: LevelMatrices, bc,
+                 radius, basis: DGBasis, force_slow: bool = False):
+    """Hybrid SLDG update of one pencil batched over leading axes (vsweep.py:173-246).
+
+    Runs the device sweep of a one-pencil plan (the same kernels as advect_velocity:
+    whole-pencil fast path, per-cell fast path, slow path); the batch becomes the
+    plan's columns.  The level matrices are rebuilt on the device from
+    (speed, dt, base width), i.e. `lm` must be precompute_level_matrices(basis, speed,
+    dt, ...) as in the reference; only its level count is read.
+    """
+    import torch
+
+    from ._device import device
+    check_bc(bc)
+    values = np.asarray(values, dtype=float)
+    lowers = np.ascontiguousarray(np.asarray(lowers, dtype=np.float64))
+    widths = np.ascontiguousarray(np.asarray(widths, dtype=np.float64))
+    levels = np.ascontiguousarray(np.asarray(levels, dtype=np.int64))
+    conforming = np.asarray(conforming, dtype=bool)
+    n, o = len(lowers), basis.n_nodes
+    if values.shape[-2:] != (n, o):
+        raise SweepError(f"pencil values shaped {values.shape[-2:]}, expected ({n}, {o})")
+    lead = values.shape[:-2]
+    nb = int(np.prod(lead)) if lead else 1
+    if nb == 0 or n == 0:
+        return np.zeros(values.shape)
+    base_width = float(widths[0] * 2.0 ** int(levels[0]))
+    arrays = dict(offsets=np.array([0, n], dtype=np.int64), group=np.zeros(1, dtype=np.int64),
+                  cell_ids=np.arange(n, dtype=np.int64), lowers=lowers, widths=widths,
+                  levels=levels, conforming=conforming.astype(np.uint8),
+                  weights=np.ones(n, dtype=np.float64))
+    n_levels = max(len(lm.n_shift), int(levels.max()) + 1)
+    plan = SweepPlan(0, basis, float(radius), base_width, n_levels, n * o, [], 1, n, arrays)
+    dev = device()
+    # state layout (rows = cell*o + node, columns = batch)
+    f = torch.from_numpy(np.ascontiguousarray(values.reshape(nb, n * o).T)).to(dev)
+    out = torch.empty_like(f)
+    sp = torch.full((nb,), float(speed), dtype=torch.float64, device=dev)
+    scratch = torch.empty(max(plan.scratch_bytes(nb), 256), dtype=torch.uint8, device=dev)
+    from ._device import current_stream
+    _capi.check(_capi.lib().sldg_advect_v(
+        plan.device_handle(), f.data_ptr(), out.data_ptr(), nb, nb, sp.data_ptr(), float(dt),
+        _capi.BC_CODE[bc], int(bool(force_slow)), scratch.data_ptr(), current_stream()),
+        SweepError)
+    return out.cpu().numpy().T.reshape(values.shape)
+
+
 def advect_velocity_into(f_in, f_out, speeds, dt, plan: SweepPlan, bc=ABSORBING,
                          force_slow=False):
     """Device-resident sweep f_out = V(f_in) (torch CUDA fp64 buffers, no host sync)."""

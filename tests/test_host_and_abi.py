@@ -112,3 +112,37 @@ def test_fit_damping_rate():
     assert not mono.ok and mono.rate is None
     y = np.array([0.0, 1.0, 1.0, 0.5, 0.8, 0.2, 0.1, 0.0])
     np.testing.assert_array_equal(sv.fit_damping_rate(np.arange(8.0), y).peak_times[:1], [1.0])
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_pack_and_scatter_lines(p):
+    """pack_line / scatter_line follow tensor.py:108-122: the line along direction d at
+    transverse pair (t1, t2) of the first and second remaining directions."""
+    o = p + 1
+    perm = sv.build_permutation(sv.DGBasis(p), 3)
+    vals = np.arange(o ** 3, dtype=float) * 1.5
+    for d in range(3):
+        rest = [t for t in range(3) if t != d]
+        for t2 in range(o):
+            for t1 in range(o):
+                trip = [None, None, None]
+                trip[d], trip[rest[0]], trip[rest[1]] = np.arange(o), t1, t2
+                idx = trip[0] + o * trip[1] + o * o * trip[2]
+                assert np.array_equal(sv.pack_line(vals, perm, d, t1, t2), vals[idx])
+                out = np.zeros_like(vals)
+                sv.scatter_line(vals[idx], out, perm, d, t1, t2)
+                assert np.array_equal(out[idx], vals[idx])
+
+
+def test_dump_mesh_csv(tmp_path):
+    m = sv.build_mesh(3, 3, 1, 6.0)
+    path = tmp_path / "mesh.csv"
+    sv.dump_mesh(m, path)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "cell,level,lo_0,lo_1,lo_2,h_0,h_1,h_2"
+    assert len(lines) == m.n_cells + 1
+    for i in (0, m.n_cells // 2, m.n_cells - 1):
+        f = lines[i + 1].split(",")
+        assert int(f[0]) == i and int(f[1]) == int(m.levels[i])
+        assert [float(x) for x in f[2:5]] == list(m.lo[i])
+        assert [float(x) for x in f[5:8]] == list(m.width[i])
