@@ -133,3 +133,16 @@ def classify_conforming(pset: PencilSet, mesh: VelocityMesh, bc: str = "absorbin
     conf[ln == 1] = False
     pset.conforming = conf
     return pset
+
+
+def dump_pencils(pset: PencilSet, path) -> None:
+    """Pencil entries as CSV (pencil, cell, lower, width, weight, conforming), %.17e
+    floats (pencil.py:171-182)."""
+    with open(path, "w", newline="\n") as fh:
+        fh.write("pencil,cell,lower,width,weight,conforming\n")
+        for q in range(pset.n_pencils):
+            sl = pset.pencil_slice(q)
+            for k in range(sl.start, sl.stop):
+                fh.write(f"{q},{int(pset.cell_ids[k])},{pset.lowers[k]:.17e},"
+                         f"{pset.widths[k]:.17e},{pset.weights[k]:.17e},"
+                         f"{int(pset.conforming[k])}\n")

@@ -25,6 +25,24 @@ def check_bc(bc: str) -> str:
     return bc
 
 
+def shifted_source(values: np.ndarray, k: int, bc: str) -> np.ndarray:
+    """out[..., i, :] = values[..., i - k, :] (sldg1d.py:103-121): a wrap (periodic) or a
+    zero-filled shift (absorbing) of the cell axis -- index bookkeeping of the
+    reference's apply_update, which itself runs on the device here."""
+    values = np.asarray(values)
+    n = values.shape[-2]
+    if bc == PERIODIC:
+        return np.roll(values, k, axis=-2)
+    if k == 0:
+        return values
+    out = np.zeros_like(values)
+    if 0 < k < n:
+        out[..., k:, :] = values[..., :n - k, :]
+    elif 0 < -k < n:
+        out[..., :n + k, :] = values[..., -k:, :]
+    return out
+
+
 @dataclass(frozen=True)
 class ShiftDecomposition:
     n_shift: int

@@ -146,3 +146,22 @@ def test_dump_mesh_csv(tmp_path):
         assert int(f[0]) == i and int(f[1]) == int(m.levels[i])
         assert [float(x) for x in f[2:5]] == list(m.lo[i])
         assert [float(x) for x in f[5:8]] == list(m.width[i])
+
+
+def test_dump_pencils_and_shifted_source(tmp_path):
+    m = sv.build_mesh(3, 3, 1, 6.0)
+    ps = sv.classify_conforming(sv.extract_pencils(m, 0), m, "absorbing")
+    from paper_2603_19959_b200.pencil import dump_pencils
+    from paper_2603_19959_b200.sldg1d import shifted_source
+    path = tmp_path / "pencils.csv"
+    dump_pencils(ps, path)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "pencil,cell,lower,width,weight,conforming"
+    assert len(lines) == len(ps.cell_ids) + 1
+    v = np.arange(2 * 5 * 3, dtype=float).reshape(2, 5, 3)
+    for k in (-6, -2, 0, 3, 5):
+        per = shifted_source(v, k, "periodic")
+        ab = shifted_source(v, k, "absorbing")
+        for i in range(5):
+            assert np.array_equal(per[:, i], v[:, (i - k) % 5])
+            assert np.array_equal(ab[:, i], v[:, i - k] if 0 <= i - k < 5 else 0 * v[:, i])
