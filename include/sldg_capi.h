@@ -229,9 +229,12 @@ int sldg_step_fused(const sldg_vplan* vplan, const sldg_xplan* xplan, const doub
  * matrices for speeds = e into `scratch`; rho_in != NULL uses that rho instead.
  * sldg_step_fused_deferred is sldg_step_fused with those level matrices and with
  * the moment / rho partials left in `scratch` for the next sldg_field_chain
- * (mom_out3 != NULL folds the moments right away).  final_x = 1 is the last step
- * of a run: f_out = X(V(f_in)), the state after the full step (no next leading
- * half step, no rho).  Results are bitwise identical to the separate calls. */
+ * (mom_out3 != NULL folds the moments right away).  mode 0 = steady state;
+ * mode 1 = the last step of a run: f_out = X(V(f_in)), the state after the full
+ * step (no next leading half step, no rho); mode 2 = the first (leading) half
+ * x-step alone, f_out = X(f_in) with rho partials (speeds unused) -- the same tile
+ * distribution, for pencil sharding.  Results are bitwise identical to the
+ * separate calls (mode 2: rho in a different summation order). */
 int sldg_field_chain(const sldg_vplan* vplan, const sldg_xplan* xplan, const sldg_poisson* p,
                      int64_t n_cols, int64_t ld, double dt, const double* rho_in, double* rho,
                      double* phi, double* e, double* diag2, double* mom_prev3, void* scratch,
@@ -239,8 +242,22 @@ int sldg_field_chain(const sldg_vplan* vplan, const sldg_xplan* xplan, const sld
 int sldg_step_fused_deferred(const sldg_vplan* vplan, const sldg_xplan* xplan,
                              const double* f_in, double* f_out, int64_t ld, int64_t n_cols,
                              const double* speeds, int32_t bc, const double* w, const double* v0,
-                             const double* v2, const double* xw, int32_t final_x,
-                             double* mom_out3, void* scratch, void* stream);
+                             const double* v2, const double* xw, int32_t mode,
+                             double* mom_out3, int64_t tile_begin, int64_t tile_count,
+                             void* scratch, void* stream);
+/* Pencil sharding: the work of one fused step is n_tiles tiles (pencil x line
+ * group x cell, in plan walk order); tile_begin/tile_count of the deferred step
+ * restrict it to one rank's contiguous share (tile_count = -1: all).  Rows outside
+ * the share are not touched.  sldg_step_fused_tiles: info[4] = {n_tiles, rows per
+ * tile, line groups per cell, cells per pencil}; tile t is cell t % cells of item
+ * t / cells, item = walk pencil x line groups + line group.  sldg_step_fused_fold
+ * folds the partials of the last deferred step (modes 0 and 2) into rho_out
+ * (n_cols) / mom_out3 (either may be NULL), in sldg_field_chain's fold order. */
+int sldg_step_fused_tiles(const sldg_vplan* vplan, const sldg_xplan* xplan, int64_t n_cols,
+                          int64_t ld, int64_t* info);
+int sldg_step_fused_fold(const sldg_vplan* vplan, const sldg_xplan* xplan, int64_t n_cols,
+                         int64_t ld, double* rho_out, double* mom_out3, void* scratch,
+                         void* stream);
 
 /* ---------------------------------------------------------------- misc */
 /* out[i*ld + j] = a[i] * b[j]: the separable initial condition sampled on the

@@ -81,7 +81,12 @@ _SIGS = {
     "sldg_step_fused_deferred": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                            C.c_int64, C.c_int64, C.c_void_p, C.c_int32,
                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                           C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+                                           C.c_int32, C.c_void_p, C.c_int64, C.c_int64,
+                                           C.c_void_p, C.c_void_p]),
+    "sldg_step_fused_tiles": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                        c_int64_p]),
+    "sldg_step_fused_fold": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                       C.c_void_p, C.c_void_p, C.c_void_p]),
     "sldg_outer": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                              C.c_int64, C.c_void_p]),
     "sldg_overlap_pairs": (C.c_int, [C.POINTER(SldgBasis), C.c_void_p, C.c_int64, C.c_void_p,

@@ -91,14 +91,17 @@ struct ItemTabs {
 
 // NXC > 0: the row length (x cells) is a compile-time constant, so every shared
 // memory offset folds into the instruction (the headline configuration).
-// FINAL: last step of a run -- X1's result is the state (stored to HBM), no X2
-// (a template flag: a runtime flag costs the steady-state kernel ~3%).
-template <int OV, int OX, int LG, int NXC, bool FINAL>
+// MODE (a template flag: a runtime flag costs the steady-state kernel ~3%):
+//   0 steady state: V + X1 (+ moments) + X2 (+ rho), as described above;
+//   1 last step of a run: V + X1 (+ moments), X1's result is the state (-> HBM);
+//   2 lead: the first half x-step alone, X1 (+ rho) -> HBM (no V) -- the tile
+//     distribution of the other modes, so a pencil-sharded rank touches only its rows.
+template <int OV, int OX, int LG, int NXC, int MODE>
 __global__ void __launch_bounds__(384, 1)
 k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout,
              int n_cols_arg, int n_xc_arg, const double* __restrict__ speeds, int bc,
              const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats, int rw_arg,
-             int n_speeds, int nmax, long long n_tiles, FusedArgs fa) {
+             int n_speeds, int nmax, long long t_begin, long long n_tiles, FusedArgs fa) {
   const int n_xc = NXC > 0 ? NXC : n_xc_arg;
   const int n_cols = NXC > 0 ? OX * NXC : n_cols_arg;
   const int rw = NXC > 0 ? ((OX * NXC) | 1) : rw_arg;
@@ -127,8 +130,16 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
 
   const int tid = threadIdx.x;
   const int nthr = blockDim.x;
-  const long long tb = (long long)blockIdx.x * n_tiles / gridDim.x;
-  const long long te = (long long)(blockIdx.x + 1) * n_tiles / gridDim.x;
+  // this CTA's share of the tile range [t_begin, t_begin + n_tiles) (a rank's
+  // pencils under pencil sharding; everything otherwise)
+  const long long tb = t_begin + (long long)blockIdx.x * n_tiles / gridDim.x;
+  const long long te = t_begin + (long long)(blockIdx.x + 1) * n_tiles / gridDim.x;
+  if (te <= tb) {   // empty share: zero partials keep the folds over the grid valid
+    grid_dep_wait();   // the preceding field chain may still be folding the partials
+    for (int k = tid; k < n_cols_arg; k += nthr) fa.rho_part[(long long)blockIdx.x * n_cols_arg + k] = 0.0;
+    if (tid < 3) fa.mom_part[blockIdx.x * 3 + tid] = 0.0;
+    return;
+  }
   const long long it_first = tb / nmax, it_last = (te - 1) / nmax;   // item range (inclusive)
   const int n_items = (int)(it_last - it_first + 1);
 
@@ -210,7 +221,8 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   grid_dep_wait();
   // ---- V-phase state: thread = column; a level is streamable when every moving
   // column's integer shift is -1 or 0 (sources in cells s-1, s, s+1)
-  const double speed = colv ? __ldg(speeds + c) : 0.0;
+  // (lead mode has no v-sweep: every column takes the copy path)
+  const double speed = (colv && MODE != 2) ? __ldg(speeds + c) : 0.0;
   if (colv && speed != 0.0) {
     for (int L = 0; L < P.n_levels; ++L) {
       const long long v = lm_ns[(long long)L * n_cols + c];
@@ -414,19 +426,24 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       if (has_next && n_staged < 3) stage(n_staged, b ^ 1, it + 1);
       ++n_staged;
       // ===================== X1 (trailing half step): stA -> stB (or HBM for the
-      // last step of a run), moments
-      auto x1 = [&](auto to_hbm) {
-        constexpr bool HBM = decltype(to_hbm)::value;
+      // last step of a run), moments; lead mode: the half step of the first step,
+      // -> HBM, rho
+      if (xv) {
 #pragma unroll
         for (int t = 0; t < LG; ++t) {
           const int r = t * OV + iv;
           double y[OX];
           xapply(stA + r * rw, y);
-          const double wr = mcur[r], wv0 = wr * mcur[R + r], wv2 = wr * mcur[2 * R + r];
-          double z = xws[cx * OX] * y[0];
+          const double wr = mcur[r];
+          double z = 0.0, wv0 = 0.0, wv2 = 0.0;
+          if (MODE != 2) {
+            wv0 = wr * mcur[R + r];
+            wv2 = wr * mcur[2 * R + r];
+            z = xws[cx * OX] * y[0];
 #pragma unroll
-          for (int k = 1; k < OX; ++k) z = fma(xws[cx * OX + k], y[k], z);
-          if (HBM) {
+            for (int k = 1; k < OX; ++k) z = fma(xws[cx * OX + k], y[k], z);
+          }
+          if (MODE != 0) {
             double* o = fout + (r0 + r) * n_cols + cx * OX;
 #pragma unroll
             for (int k = 0; k < OX; ++k) o[k] = y[k];
@@ -435,19 +452,21 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
 #pragma unroll
             for (int k = 0; k < OX; ++k) o[k] = y[k];
           }
-          m0 = fma(wr, z, m0);
-          m1 = fma(wv0, z, m1);
-          m2 = fma(wv2, z, m2);
+          if (MODE == 2) {
+#pragma unroll
+            for (int k = 0; k < OX; ++k) rha[k] = fma(wr, y[k], rha[k]);
+          } else {
+            m0 = fma(wr, z, m0);
+            m1 = fma(wv0, z, m1);
+            m2 = fma(wv2, z, m2);
+          }
         }
-      };
-      if (xv) {
-        x1(BoolC<FINAL>{});
       }
       __syncthreads();
       // ===================== X2 (next step's leading half): stB -> HBM, rho
       // No barrier after X2: the next V writes stA (last read in X1, before the
       // barrier above) and the ring slot it refills was last read in this V.
-      if (xv && !FINAL) {
+      if (xv && MODE == 0) {
         double* dst = fout + (r0 + iv) * n_cols + cx * OX;
 #pragma unroll
         for (int t = 0; t < LG; ++t) {
@@ -572,33 +591,35 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
 
 using FusedKernel = void (*)(VPlanDev, XPlanDev, const double*, double*, int, int, const double*,
                              int, const long long*, const double*, int, int, int, long long,
-                             FusedArgs);
+                             long long, FusedArgs);
 
-template <int OV, int OX, bool FINAL>
-static FusedKernel pick_kernel_f(int lg, long long n_xc) {
+template <int OV, int OX, int MODE>
+static FusedKernel pick_kernel_m(int lg, long long n_xc) {
   if (lg == OV) {
     if constexpr (OV == 3 && OX == 3) {
-      if (n_xc == 64) return k_step_fused<3, 3, 3, 64, FINAL>;
+      if (n_xc == 64) return k_step_fused<3, 3, 3, 64, MODE>;
     }
-    return k_step_fused<OV, OX, OV, 0, FINAL>;
+    return k_step_fused<OV, OX, OV, 0, MODE>;
   }
   if constexpr (OV % 2 == 0 && OV != 2) {
-    if (lg == 2) return k_step_fused<OV, OX, 2, 0, FINAL>;
+    if (lg == 2) return k_step_fused<OV, OX, 2, 0, MODE>;
   }
-  if (lg == 1) return k_step_fused<OV, OX, 1, 0, FINAL>;
+  if (lg == 1) return k_step_fused<OV, OX, 1, 0, MODE>;
   return nullptr;
 }
 
 template <int OV, int OX>
-static FusedKernel pick_kernel(int lg, long long n_xc, bool final_x) {
-  return final_x ? pick_kernel_f<OV, OX, true>(lg, n_xc) : pick_kernel_f<OV, OX, false>(lg, n_xc);
+static FusedKernel pick_kernel(int lg, long long n_xc, int mode) {
+  if (mode == 1) return pick_kernel_m<OV, OX, 1>(lg, n_xc);
+  if (mode == 2) return pick_kernel_m<OV, OX, 2>(lg, n_xc);
+  return pick_kernel_m<OV, OX, 0>(lg, n_xc);
 }
 
 static FusedKernel fused_kernel(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
-                                bool final_x = false) {
+                                int mode = 0) {
   switch (vp->o * 10 + xp->o) {
 #define CASE(A, B) \
-  case A * 10 + B: return pick_kernel<A, B>(g.lg, xp->n_cells, final_x);
+  case A * 10 + B: return pick_kernel<A, B>(g.lg, xp->n_cells, mode);
     CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(4, 2) CASE(4, 3)
     CASE(4, 4)
 #undef CASE
@@ -836,13 +857,21 @@ int check_geom(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_cols, int64
 
 int launch_step(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g, const double* fin,
                 double* fout, int64_t n_cols, const double* speeds, int32_t bc,
-                const FusedScratch& s, const FusedArgs& fa, int final_x, cudaStream_t st,
-                long long* grid) {
+                const FusedScratch& s, const FusedArgs& fa, int mode, cudaStream_t st,
+                long long* grid, long long t_begin = 0, long long t_count = -1) {
   if ((((unsigned long long)fin) & 15) != 0 || n_cols % 2 != 0) {
     set_error("fused step: 16-byte aligned rows required");
     return SLDG_ERR_UNSUPPORTED;
   }
-  FusedKernel k = fused_kernel(vp, xp, g, final_x != 0);
+  if (t_count < 0) {
+    t_begin = 0;
+    t_count = g.n_tiles;
+  }
+  if (t_begin < 0 || t_begin + t_count > g.n_tiles) {
+    set_error("fused step: tile range outside the plan");
+    return SLDG_ERR_ARG;
+  }
+  FusedKernel k = fused_kernel(vp, xp, g, mode);
   if (!k) {
     set_error("fused step: no kernel for this degree / line group");
     return SLDG_ERR_UNSUPPORTED;
@@ -852,7 +881,7 @@ int launch_step(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g, 
   SLDG_CUDA_TRY(launch_pdl(k, dim3((unsigned)*grid), dim3(g.threads), g.smem, st, vp->dev,
                            xp->dev, fin, fout, (int)n_cols, (int)xp->n_cells, speeds, (int)bc,
                            (const long long*)s.lm_ns, (const double*)s.lm_mats, g.rw,
-                           (int)xp->n_speeds, g.nmax, g.n_tiles, fa));
+                           (int)xp->n_speeds, g.nmax, t_begin, t_count, fa));
   SLDG_LAUNCH_CHECK("k_step_fused");
   return SLDG_OK;
 }
@@ -912,10 +941,11 @@ int sldg_step_fused(const sldg_vplan* vp, const sldg_xplan* xp, const double* fi
 int sldg_step_fused_deferred(const sldg_vplan* vp, const sldg_xplan* xp, const double* fin,
                              double* fout, int64_t ld, int64_t n_cols, const double* speeds,
                              int32_t bc, const double* w, const double* v0, const double* v2,
-                             const double* xw, int32_t final_x, double* mom_out3, void* scratch,
+                             const double* xw, int32_t mode, double* mom_out3,
+                             int64_t tile_begin, int64_t tile_count, void* scratch,
                              void* stream) {
   if (bad_step_args(vp, xp, fin, fout, speeds, bc, w, v0, v2, xw, scratch) ||
-      (final_x != 0 && final_x != 1)) {
+      (mode < 0 || mode > 2)) {
     set_error("bad sldg_step_fused_deferred arguments");
     return SLDG_ERR_ARG;
   }
@@ -926,10 +956,58 @@ int sldg_step_fused_deferred(const sldg_vplan* vp, const sldg_xplan* xp, const d
   cudaStream_t st = (cudaStream_t)stream;
   long long grid = 0;
   rc = launch_step(vp, xp, g, fin, fout, n_cols, speeds, bc, s,
-                   FusedArgs{w, v0, v2, xw, s.mom_part, s.rho_part}, final_x, st, &grid);
+                   FusedArgs{w, v0, v2, xw, s.mom_part, s.rho_part}, mode, st, &grid,
+                   tile_begin, tile_count);
   if (rc || !mom_out3) return rc;
   k_fold3<<<1, 96, 0, st>>>(s.mom_part, grid, mom_out3);
   SLDG_LAUNCH_CHECK("k_fold3");
+  return SLDG_OK;
+}
+
+int sldg_step_fused_tiles(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_cols, int64_t ld,
+                          int64_t* info) {
+  if (!vp || !xp || !info) {
+    set_error("null argument");
+    return SLDG_ERR_ARG;
+  }
+  FusedGeom g;
+  int rc = check_geom(vp, xp, n_cols, ld, &g);
+  if (rc) return rc;
+  info[0] = g.n_tiles;
+  info[1] = (int64_t)g.lg * vp->o;   // rows per tile
+  info[2] = g.n_lg;                  // line groups per cell
+  info[3] = g.nmax;                  // cells per item (pencil length)
+  return SLDG_OK;
+}
+
+int sldg_step_fused_fold(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_cols, int64_t ld,
+                         double* rho_out, double* mom_out3, void* scratch, void* stream) {
+  if (!vp || !xp || !scratch || (!rho_out && !mom_out3)) {
+    set_error("bad sldg_step_fused_fold arguments");
+    return SLDG_ERR_ARG;
+  }
+  FusedGeom g;
+  int rc = check_geom(vp, xp, n_cols, ld, &g);
+  if (rc) return rc;
+  FusedKernel k = fused_kernel(vp, xp, g);
+  if (!k) {
+    set_error("fused step: no kernel for this degree / line group");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  long long grid = 0;
+  rc = fused_grid(k, g, &grid);
+  if (rc) return rc;
+  const FusedScratch s = fused_scratch(vp, g, n_cols, scratch);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (mom_out3) {
+    k_fold3<<<1, 96, 0, st>>>(s.mom_part, grid, mom_out3);
+    SLDG_LAUNCH_CHECK("k_fold3");
+  }
+  if (rho_out) {
+    k_fold_cols<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>(s.rho_part, grid, n_cols,
+                                                                        rho_out);
+    SLDG_LAUNCH_CHECK("k_fold_cols");
+  }
   return SLDG_OK;
 }
 

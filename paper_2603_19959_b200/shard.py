@@ -27,6 +27,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .driver import Simulation
 from .sldg1d import decompose_shift
 
 
@@ -314,3 +315,114 @@ class ShardedSimulation:
         r = self._rec.cpu().numpy()
         return DiagnosticsRecord(self.t, float(r[0]), float(r[2]), float(r[3]), float(r[4]),
                                  float(r[1]), 0.5 * float(r[4]) + float(r[1]))
+
+
+class PencilShardedSimulation(Simulation):
+    """Pencil sharding for the plans the fused step covers (uniform velocity meshes).
+
+    For those plans a direction-0 pencil's cells are swept together and every
+    x row belongs to exactly one (pencil, line group, cell) tile of k_step_fused,
+    so the whole Strang step -- leading half-x, v-sweep, trailing half-x -- is
+    local to a (pencil, line group) item.  Each rank holds the full state buffer but
+    advances only its contiguous share of whole items (rows of other ranks are never
+    read or written here); the only exchange per step is the rank's partial sums
+    [rho (N_x^DOF) | m0 m1 m2], added in rank order on every rank
+    (sum_in_rank_order) so all ranks solve the same Poisson problem.  Total work
+    is fixed as ranks are added (strong scaling).
+
+    `reducer(vec) -> vec` replaces the cross-rank sum (tests run ranks in lockstep
+    on one device).
+    """
+
+    def __init__(self, config, rank, world, group=None, mesh=None, reducer=None):
+        super().__init__(config, mesh=mesh)
+        if not self.fused_step_supported():
+            raise ValueError("pencil sharding needs a plan the fused step covers "
+                             "(uniform velocity mesh)")
+        import torch
+
+        from . import _capi
+        info = np.zeros(4, dtype=np.int64)
+        _capi.check(_capi.lib().sldg_step_fused_tiles(
+            self.sweep_plan.device_handle(), self.x_plan.device_handle(), self._f.shape[1],
+            self._f.stride(0), _capi.i64ptr(info)), ValueError)
+        self.n_tiles, self.rows_per_tile, self.line_groups, self.cells_per_pencil = \
+            (int(v) for v in info)
+        # whole items only: the v-sweep of a cell reads its pencil neighbours, which
+        # must be rows this rank keeps current
+        n_items = self.n_tiles // self.cells_per_pencil
+        i0, i1 = rank * n_items // world, (rank + 1) * n_items // world
+        self._tile_range = (i0 * self.cells_per_pencil, (i1 - i0) * self.cells_per_pencil)
+        self.rank, self.world, self.group = rank, world, group
+        self._reducer = reducer if reducer is not None else \
+            (lambda v: sum_in_rank_order(v, group))
+        self._part = torch.zeros(self._f.shape[1] + 3, dtype=torch.float64,
+                                 device=self._f.device)
+
+    def owned_rows(self) -> np.ndarray:
+        """Rows of f this rank advances: the rows of its tiles (tile t = cell
+        t % cells of item t // cells; item = pencil * line_groups + line group)."""
+        a = self.sweep_plan._arrays
+        t = np.arange(*((self._tile_range[0], self._tile_range[0] + self._tile_range[1])))
+        cell = t % self.cells_per_pencil
+        item = t // self.cells_per_pencil
+        pencil, lgrp = item // self.line_groups, item % self.line_groups
+        cid = a["cell_ids"][a["offsets"][pencil] + cell]
+        base = cid * self.sweep_plan.n_dofs // self.sweep_plan.n_cells + lgrp * self.rows_per_tile
+        return (base[:, None] + np.arange(self.rows_per_tile)[None, :]).ravel()
+
+    # phases ----------------------------------------------------------------
+    def _fold_partials(self, moments: bool):
+        """This rank's [rho | m0 m1 m2] from the partials of its last deferred step."""
+        from . import _capi
+        from ._device import SCRATCH, current_stream
+        n = self._f.shape[1]
+        scratch = SCRATCH.get(("fused", id(self)), self._fused_bytes)
+        if not moments:
+            self._part[n:].zero_()
+        _capi.check(_capi.lib().sldg_step_fused_fold(
+            self.sweep_plan.device_handle(), self.x_plan.device_handle(), n, self._f.stride(0),
+            self._part[:n].data_ptr(), self._part[n:].data_ptr() if moments else None,
+            scratch.data_ptr(), current_stream()), ValueError)
+        return self._part
+
+    def _take_sums(self, tot, mom3=None):
+        n = self._f.shape[1]
+        self._rho.copy_(tot[:n])
+        if mom3 is not None:
+            mom3.copy_(tot[n:])
+
+    def advance(self, n_steps: int, table=None, v_events=None):
+        """n_steps pipelined Strang steps on this rank's tiles; row k of the returned
+        table is step k's [max|E|, e_field, m0, m1, m2] (global, identical on all ranks)."""
+        import torch
+        if table is None:
+            table = torch.empty((n_steps, 5), dtype=torch.float64, device=self._f.device)
+        if n_steps == 0:
+            return table
+        e = self._e
+        n = self._f.shape[1]
+        # leading half x-step of step 0 on my tiles, rho summed over the ranks
+        self._fused_step_deferred(e, mode=2)
+        self._take_sums(self._reducer(self._fold_partials(False).clone()))
+        for k in range(n_steps):
+            self._field_chain(e, table[k, 0:2], None)   # Poisson, E, diagnostics, level mats
+            if v_events is not None:
+                v_events[k][0].record(torch.cuda.current_stream())
+            last = k + 1 == n_steps
+            if last:
+                self._fused_step_deferred(e, final=True, mom_out3=self._part[n:])
+                self._part[:n].zero_()
+                table[k, 2:5].copy_(self._reducer(self._part.clone())[n:])
+            else:
+                self._fused_step_deferred(e)
+                self._take_sums(self._reducer(self._fold_partials(True).clone()), table[k, 2:5])
+            if v_events is not None:
+                v_events[k][1].record(torch.cuda.current_stream())
+        return table
+
+    def step(self):
+        """One Strang step (the pipelined path with n_steps = 1)."""
+        table = self.advance(1)
+        self.t += self.config.dt
+        return self._record(self.t, table[0])
