@@ -317,6 +317,15 @@ class ShardedSimulation:
                                  float(r[1]), 0.5 * float(r[4]) + float(r[1]))
 
 
+def item_tile_range(n_tiles: int, cells_per_item: int, rank: int, world: int):
+    """(first tile, tile count) of `rank`'s contiguous share of whole items: the
+    v-sweep of a cell reads its pencil neighbours, which must be rows the same rank
+    keeps current, so items are never split between ranks."""
+    n_items = n_tiles // cells_per_item
+    i0, i1 = rank * n_items // world, (rank + 1) * n_items // world
+    return i0 * cells_per_item, (i1 - i0) * cells_per_item
+
+
 class PencilShardedSimulation(Simulation):
     """Pencil sharding for the plans the fused step covers (uniform velocity meshes).
 
@@ -348,11 +357,7 @@ class PencilShardedSimulation(Simulation):
             self._f.stride(0), _capi.i64ptr(info)), ValueError)
         self.n_tiles, self.rows_per_tile, self.line_groups, self.cells_per_pencil = \
             (int(v) for v in info)
-        # whole items only: the v-sweep of a cell reads its pencil neighbours, which
-        # must be rows this rank keeps current
-        n_items = self.n_tiles // self.cells_per_pencil
-        i0, i1 = rank * n_items // world, (rank + 1) * n_items // world
-        self._tile_range = (i0 * self.cells_per_pencil, (i1 - i0) * self.cells_per_pencil)
+        self._tile_range = item_tile_range(self.n_tiles, self.cells_per_pencil, rank, world)
         self.rank, self.world, self.group = rank, world, group
         self._reducer = reducer if reducer is not None else \
             (lambda v: sum_in_rank_order(v, group))

@@ -129,3 +129,17 @@ def test_partition_and_halo_widths():
     with pytest.raises(ValueError):
         shard.HaloExchanger(0, 2, 5, 1, 3, 4)
     assert shard.margin_dofs(3, 3) == 10 and shard.margin_dofs(2, 3) == 6
+
+
+@pytest.mark.parametrize("n_items,cells,world", [(3072, 32, 8), (50, 5, 3), (7, 4, 8), (9, 2, 2)])
+def test_pencil_item_ranges_cover_whole_items(n_items, cells, world):
+    """Pencil sharding: the ranks' tile shares are contiguous, disjoint, cover every
+    tile, start and end on item boundaries, and differ by at most one item."""
+    spans = [shard.item_tile_range(n_items * cells, cells, r, world) for r in range(world)]
+    pos = 0
+    for t0, cnt in spans:
+        assert t0 == pos and t0 % cells == 0 and cnt % cells == 0
+        pos += cnt
+    assert pos == n_items * cells
+    sizes = [c // cells for _, c in spans]
+    assert max(sizes) - min(sizes) <= 1
