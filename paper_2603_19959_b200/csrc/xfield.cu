@@ -471,6 +471,10 @@ static XTGeom xt_geom(const sldg_xplan* X) {
   }
   if (!g.ok) return g;
   g.n_tiles = (X->n_rows / nloc) * (nl / g.rpt) * ov;
+  if (g.n_tiles * g.tpc >= (1LL << 31)) {   // the kernel indexes tiles in 32 bits
+    g.ok = false;
+    return g;
+  }
   g.n_groups = (g.n_tiles + g.tpc - 1) / g.tpc;
   const long long ctas_sm = std::max<long long>(1, std::min<long long>(
       (long long)(227 * 1024 / g.smem), 2048 / g.threads));

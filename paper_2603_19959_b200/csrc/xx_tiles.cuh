@@ -49,8 +49,9 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
   const int cx = tid - tt * n_xc;            // x cell
   const bool act = tt < tpc;
   const int per_cell = (NL / rpt) * OV;      // tiles per velocity cell
-  const long long n_tiles = (n_rows / NLOC) * per_cell;
-  const long long n_groups = (n_tiles + tpc - 1) / tpc;
+  // tile and group indices fit in 32 bits (the host checks n_tiles < 2^31)
+  const int n_tiles = (int)((n_rows / NLOC) * per_cell);
+  const int n_groups = (n_tiles + tpc - 1) / tpc;
   const int slot_dbl = tpc * rpt * row_len;
   double* ring = sm;
   double* mid = ring + (long long)nring * slot_dbl;
@@ -66,11 +67,11 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
   for (int k = tid; k < n_speeds; k += blockDim.x) xnsm[k] = X.ident[k] ? 0 : __ldg(X.nsm + k);
 
   // tile id -> first row and row stride (rows u = 0..rpt-1 are row0 + u*OV)
-  auto tile_row0 = [&](long long tile) -> long long {
-    const long long cell = tile / per_cell;
-    const int rem = (int)(tile - cell * per_cell);
+  auto tile_row0 = [&](int tile) -> long long {
+    const int cell = tile / per_cell;
+    const int rem = tile - cell * per_cell;
     const int iv = rem % OV, tg = rem / OV;
-    return cell * NLOC + (long long)tg * rpt * OV + iv;
+    return (long long)cell * NLOC + tg * rpt * OV + iv;
   };
 
   // a slot is full when warp 0's bulk copies have landed and (epilogues) warp 1's
@@ -82,16 +83,14 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
   }
   __syncthreads();
 
-  const long long g0 = blockIdx.x, gs = gridDim.x;
-  const long long my = g0 < n_groups ? (n_groups - g0 + gs - 1) / gs : 0;
-  // issue group i (of this CTA) into slot i % nring: one bulk copy per row (warp 0),
-  // metadata (w, v0, v2 of each row) by cp.async from warp 1 into the slot's meta
+  const int g0 = blockIdx.x, gs = gridDim.x;
+  const int my = g0 < n_groups ? (n_groups - g0 + gs - 1) / gs : 0;
+  // issue group i (of this CTA) into slot s = i % nring: one bulk copy per row (warp
+  // 0), metadata (w, v0, v2 of each row) by cp.async from warp 1 into the slot's meta
   // block, completion signalled on the slot's barrier (no thread waits on it)
-  auto issue = [&](long long i) {
-    const int s = (int)(i % nring);
-    const long long grp = g0 + i * gs;
-    const long long t_first = grp * tpc;
-    const int nt = (int)min((long long)tpc, n_tiles - t_first);
+  auto issue = [&](int i, int s) {
+    const int t_first = (g0 + i * gs) * tpc;
+    const int nt = min(tpc, n_tiles - t_first);
     if (tid < 32) {
       if (tid == 0) mbar_expect_tx(&full[s], (unsigned)(nt * rpt * row_len * 8));
       __syncwarp();
@@ -115,25 +114,25 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
       cp_async_arrive(&full[s]);
     }
   };
-  for (long long i = 0; i < min((long long)nring - 1, my); ++i) issue(i);
+  for (int i = 0; i < min(nring - 1, my); ++i) issue(i, i);
 
   double m0a[OX], m1a[OX], m2a[OX], rha[OX];
 #pragma unroll
   for (int k = 0; k < OX; ++k) m0a[k] = m1a[k] = m2a[k] = rha[k] = 0.0;
 
-  auto speed_of = [&](long long i) -> int {   // this thread's tile speed in group i
-    const long long tile = (g0 + i * gs) * tpc + tt;
+  auto speed_of = [&](int i) -> int {   // this thread's tile speed in group i
+    const int tile = (g0 + i * gs) * tpc + tt;
     return (act && i < my && tile < n_tiles) ? __ldg(X.row_speed + tile_row0(tile)) : 0;
   };
   int g_next = speed_of(0);
-  for (long long i = 0; i < my; ++i) {
-    if (i + nring - 1 < my) issue(i + nring - 1);
+  int s = 0, phase = 0;   // slot and barrier phase of group i (i % nring, (i / nring) & 1)
+  for (int i = 0; i < my; ++i) {
+    if (i + nring - 1 < my) issue(i + nring - 1, s == 0 ? nring - 1 : s - 1);
     const int g = g_next;
     g_next = speed_of(i + 1);                 // prefetched one group ahead
-    const int s = (int)(i % nring);
-    mbar_wait(&full[s], (unsigned)((i / nring) & 1));   // rows and metadata of slot s
-    const long long t_first = (g0 + i * gs) * tpc;
-    const long long tile = t_first + tt;
+    mbar_wait(&full[s], (unsigned)phase);     // rows and metadata of slot s
+    const int t_first = (g0 + i * gs) * tpc;
+    const int tile = t_first + tt;
     const bool live = act && tile < n_tiles;
     double xa[OX * OX], xb[OX * OX];
     int ia = 0, ib = 0;
@@ -217,6 +216,10 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
       }
     }
     __syncthreads();                          // slot s and mid are reused next
+    if (++s == nring) {
+      s = 0;
+      phase ^= 1;
+    }
   }
 
   // CTA partials: rho per column (tiles of the group summed in order), moments
