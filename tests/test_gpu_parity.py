@@ -463,3 +463,31 @@ def test_sweep_other_directions_vs_oracle(direction, nb, lv, p, bc):
     got = fd.cpu().numpy()
     assert np.abs(got - ref).max() <= TOL * np.abs(ref).max()
     assert np.array_equal(got[:, 2], f[:, 2])
+
+
+@pytest.mark.parametrize("bc", ["absorbing", "periodic"])
+@pytest.mark.parametrize("emax", [0.02, 9.0, 40.0])
+def test_fused_step_any_shift_matches_separate_passes(bc, emax):
+    """k_step_fused with E large enough that the v-shift leaves {-1, 0} (the kernel's
+    global-load path instead of the TMA ring) == advect_v followed by the X.X pass."""
+    kw = dict(dim=3, n_base=6, levels=0, degree=2, n_x=32, bc=bc)
+    a = sv.Simulation(sv.SimConfig(**kw, n_steps=1))
+    b = sv.Simulation(sv.SimConfig(**kw, n_steps=1))
+    assert a.fused_step_supported()
+    rng = np.random.default_rng(int(emax * 10))
+    e = dev(rng.uniform(-emax, emax, a.f.shape[1]))
+    e[3] = 0.0
+    f0 = dev(rng.standard_normal(tuple(a.f.shape)))
+    a.f.copy_(f0)
+    b.f.copy_(f0)
+    out_a = torch.empty(3, dtype=torch.float64, device=DEV)
+    out_b = torch.empty(3, dtype=torch.float64, device=DEV)
+    a._fused_step(e, out_a)
+    b._advect_v(e)
+    b._xx(out_b)
+    fa, fb = a.f.cpu().numpy(), b.f.cpu().numpy()
+    assert np.abs(fa - fb).max() <= 1e-13 * np.abs(fb).max()
+    np.testing.assert_allclose(out_a.cpu().numpy(), out_b.cpu().numpy(), rtol=1e-12,
+                               atol=1e-12 * abs(float(out_b[0])))
+    np.testing.assert_allclose(a._rho.cpu().numpy(), b._rho.cpu().numpy(), rtol=1e-12,
+                               atol=1e-12 * float(b._rho.abs().max()))
