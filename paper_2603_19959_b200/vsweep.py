@@ -16,8 +16,8 @@ import numpy as np
 from . import _capi
 from .basis import DGBasis
 from .pencil import PencilSet
-from .sldg1d import (ABSORBING, PERIODIC, OverlapPair, ShiftDecomposition, check_bc,
-                     decompose_shift, overlap_pairs_device)
+from .sldg1d import (ABSORBING, PERIODIC, OverlapPair, ShiftDecomposition, check_bc,  # noqa: F401
+                     decompose_shift, overlap_pairs_device)   # (module names as in vsweep.py)
 from .tensor import TensorPermutation
 from .vmesh import VelocityMesh
 
