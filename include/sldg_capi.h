@@ -172,6 +172,20 @@ int sldg_advect_x_fused(const sldg_xplan* plan, const double* f_in, double* f_ou
 int sldg_advect_x_slab(const sldg_xplan* plan, const double* f_in, int64_t ld_in,
                        int64_t halo_l, int64_t halo_r, int64_t n_local, double* f_out,
                        int64_t ld_out, void* stream);
+/* The same slab update with the row-tile kernel (plans with a velocity layout,
+ * sldg_xplan_set_vlayout) and the fused epilogues of sldg_advect_x_fused: the rows
+ * of row_base (16-byte aligned, ld_in even) are staged whole; halo-relative cell 0
+ * starts at double src_off, local cells at halo_l..; outputs go to out_off of rows
+ * of f_out (ld_out).  rho_out: n_local*o columns; mom_out3 with xw_local (the local
+ * x weights).  scratch: sldg_advect_x_slab_tiles_scratch bytes (NULL without
+ * epilogues); SLDG_ERR_UNSUPPORTED when the plan or shape does not fit the kernel. */
+int sldg_advect_x_slab_tiles_scratch(const sldg_xplan* plan, int64_t n_local, int64_t ld_in,
+                                     size_t* bytes);
+int sldg_advect_x_slab_tiles(const sldg_xplan* plan, const double* row_base, int64_t ld_in,
+                             int64_t src_off, int64_t halo_l, int64_t n_local, double* f_out,
+                             int64_t ld_out, int64_t out_off, const double* w, const double* v0,
+                             const double* v2, const double* xw_local, double* mom_out3,
+                             double* rho_out, void* scratch, void* stream);
 
 /* rho[c] = sum_r w[r] f[r, c]  (deterministic two-stage column reduction).
  * scratch: sldg_rho_scratch_bytes(). */

@@ -121,6 +121,13 @@ _SIGS = {
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sldg_advect_x_slab": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
+    "sldg_advect_x_slab_tiles_scratch": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64,
+                                                   C.POINTER(C.c_size_t)]),
+    "sldg_advect_x_slab_tiles": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                           C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
+                                           C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_void_p]),
     "sldg_rho_scratch_bytes": (C.c_int, [C.c_int64, C.c_int64, C.POINTER(C.c_size_t)]),
     "sldg_rho": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
                            C.c_void_p, C.c_void_p]),

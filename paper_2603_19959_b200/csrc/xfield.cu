@@ -441,18 +441,22 @@ static int launch_xadv(const sldg_xplan* X, const double* fin, long long ld_in, 
 namespace sldg {
 
 // Geometry of k_xx_tiles: depends only on the problem shape (bitwise-stable sums).
-static XTGeom xt_geom(const sldg_xplan* X) {
+// n_out: output cells per row (default: the periodic row); src_len: doubles staged
+// per source row (default: the row itself; an x slab stages its margins too)
+static XTGeom xt_geom(const sldg_xplan* X, long long n_out = -1, long long src_len = -1) {
   XTGeom g{};
   g.ok = false;
   const int ov = X->vo, ox = X->o;
-  const long long nxc = X->n_cells;
+  const long long nxc = n_out < 0 ? X->n_cells : n_out;
   if (ov < 2 || ov > 4 || ox < 2 || ox > 4 || nxc > 512 || X->n_rows == 0) return g;
   const int nl = ov * ov, nloc = nl * ov;
   if (X->n_rows % nloc != 0) return g;
   g.tpc = (int)std::max<long long>(1, std::min<long long>(kXTMaxTpc, 512 / nxc));
   g.threads = (int)((g.tpc * nxc + 31) / 32 * 32);
   if (g.threads < 64) g.threads = 64;
-  const long long row_len = nxc * ox;
+  const long long row_len = src_len < 0 ? nxc * ox : src_len;
+  g.n_out = (int)nxc;
+  g.src_len = (int)row_len;
   const size_t table = sizeof(double) * X->n_speeds * 2 * ox * ox + 5 * X->n_speeds + 64;
   const size_t budget = 227 * 1024 - 1024;
   for (int nring : {3, 2}) {
@@ -486,26 +490,27 @@ static XTGeom xt_geom(const sldg_xplan* X) {
 template <int OV, int OX>
 static int launch_xt_t(const sldg_xplan* X, const XTGeom& g, const double* fin, double* fout,
                        long long ld, int napply, bool mom, bool rho, const XEpi& epi,
-                       cudaStream_t st) {
+                       cudaStream_t st, const XRowMap& rm) {
   auto k = k_xx_tiles<OV, OX, 0>;
   if constexpr (OV == 3) {
     if (g.rpt == 3) k = k_xx_tiles<OV, OX, 3>;
   }
   SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
-  k<<<(unsigned)g.grid_, g.threads, g.smem, st>>>(X->dev, fin, fout, ld, X->n_rows,
-                                                  (int)X->n_cells, g.rpt, g.tpc, g.nring,
-                                                  (int)X->n_speeds, epi, napply, mom ? 1 : 0,
-                                                  rho ? 1 : 0);
+  k<<<(unsigned)g.grid_, g.threads, g.smem, st>>>(X->dev, fin, fout, ld, X->n_rows, g.n_out,
+                                                  g.rpt, g.tpc, g.nring, (int)X->n_speeds, epi,
+                                                  napply, mom ? 1 : 0, rho ? 1 : 0, rm);
   SLDG_LAUNCH_CHECK("k_xx_tiles");
   return SLDG_OK;
 }
 
 static int launch_xt(const sldg_xplan* X, const XTGeom& g, const double* fin, double* fout,
                      long long ld, int napply, bool mom, bool rho, const XEpi& epi,
-                     cudaStream_t st) {
+                     cudaStream_t st, const XRowMap* rmap = nullptr) {
+  // default: periodic rows, output in place of the input layout
+  const XRowMap rm = rmap ? *rmap : XRowMap{g.src_len, 0, 0, 1, 0, ld};
   switch (X->vo * 10 + X->o) {
 #define CASE(A, B) \
-  case A * 10 + B: return launch_xt_t<A, B>(X, g, fin, fout, ld, napply, mom, rho, epi, st);
+  case A * 10 + B: return launch_xt_t<A, B>(X, g, fin, fout, ld, napply, mom, rho, epi, st, rm);
     CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(4, 2) CASE(4, 3)
     CASE(4, 4)
 #undef CASE
@@ -797,6 +802,63 @@ int sldg_advect_x_slab(const sldg_xplan* X, const double* fin, int64_t ld_in, in
   }
   set_error("unsupported degree");
   return SLDG_ERR_UNSUPPORTED;
+}
+
+int sldg_advect_x_slab_tiles_scratch(const sldg_xplan* X, int64_t n_local, int64_t ld_in,
+                                     size_t* bytes) {
+  if (!X || !bytes || n_local < 1) {
+    set_error("bad argument");
+    return SLDG_ERR_ARG;
+  }
+  const XTGeom tg = xt_geom(X, n_local, ld_in);
+  if (!tg.ok) {
+    set_error("slab tile kernel: unsupported shape");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  *bytes = sizeof(double) * (size_t)tg.grid_ * (3 + n_local * X->o) + 256;
+  return SLDG_OK;
+}
+
+int sldg_advect_x_slab_tiles(const sldg_xplan* X, const double* row_base, int64_t ld_in,
+                             int64_t src_off, int64_t halo_l, int64_t n_local, double* fout,
+                             int64_t ld_out, int64_t out_off, const double* w, const double* v0,
+                             const double* v2, const double* xw_local, double* mom_out3,
+                             double* rho_out, void* scratch, void* stream) {
+  const bool mom = mom_out3 != nullptr, rho = rho_out != nullptr;
+  if (!X || !row_base || !fout || n_local < 1 || halo_l < X->halo_l || src_off < 0 ||
+      src_off + (halo_l + n_local + X->halo_r) * X->o > ld_in || out_off < 0 ||
+      out_off + n_local * X->o > ld_out || (mom && (!w || !v0 || !v2 || !xw_local)) ||
+      (rho && !w) || ((mom || rho) && !scratch)) {
+    set_error("bad advect_x_slab_tiles arguments (halo too narrow?)");
+    return SLDG_ERR_ARG;
+  }
+  if (X->n_rows == 0) return SLDG_OK;
+  // whole padded rows are staged (16-byte aligned bulk copies)
+  const XTGeom tg = xt_geom(X, n_local, ld_in);
+  if (!tg.ok || (ld_in & 1) || (((unsigned long long)row_base) & 15)) {
+    set_error("slab tile kernel: unsupported shape (rows too long / unaligned)");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  XEpi epi{w, v0, v2, xw_local, nullptr, nullptr};
+  if (scratch) {
+    epi.mom_part = (double*)scratch;
+    epi.rho_part = (double*)scratch + 3 * (size_t)tg.grid_;
+  }
+  const XRowMap rm{(int)ld_in, (int)src_off, (int)halo_l, 0, (int)out_off, ld_out};
+  int rc = launch_xt(X, tg, row_base, fout, ld_in, 1, mom, rho, epi, st, &rm);
+  if (rc) return rc;
+  if (mom) {
+    k_sum3<<<1, 96, 0, st>>>(epi.mom_part, tg.grid_, mom_out3);
+    SLDG_LAUNCH_CHECK("k_sum3");
+  }
+  if (rho) {
+    const long long row_len = n_local * X->o;
+    k_colsum<<<(unsigned)((row_len * 32 + 255) / 256), 256, 0, st>>>(epi.rho_part, tg.grid_,
+                                                                row_len, rho_out);
+    SLDG_LAUNCH_CHECK("k_colsum");
+  }
+  return SLDG_OK;
 }
 
 int sldg_rho_scratch_bytes(int64_t n_rows, int64_t n_cols, size_t* bytes) {

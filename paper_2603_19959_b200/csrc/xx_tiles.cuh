@@ -24,6 +24,7 @@ namespace sldg {
 
 struct XTGeom {
   int rpt, tpc, nring, threads;   // rows per tile, tiles per CTA step, ring depth, threads
+  int n_out, src_len;             // output cells per row, staged doubles per source row
   long long n_tiles, n_groups, grid_;
   size_t smem;
   bool ok;
@@ -31,19 +32,31 @@ struct XTGeom {
 
 constexpr int kXTMaxTpc = 8;
 
+// Where a row's sources and outputs live.  Periodic rows (wrap = 1): the n_xc
+// cells of the row, sources wrap around.  x slabs (wrap = 0, the sharded state):
+// the input row is [left margin | local | right margin], src_len doubles copied
+// from the row start, halo-relative cell j at src_off + j*o, the local cells are
+// j = hl .. hl+n_xc-1 (no wrap: the halo covers every shift); outputs go to
+// out_off + cx*o of rows with stride ld_out.
+struct XRowMap {
+  int src_len, src_off, hl, wrap, out_off;
+  long long ld_out;
+};
+
 // RPT > 0: rows per tile fixed at compile time (row loops unrolled, tile -> row
 // arithmetic by constants); 0 = the geometry's value at run time.
 template <int OV, int OX, int RPT>
 __global__ void __launch_bounds__(512, 1)
 k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout, long long ld,
            long long n_rows, int n_xc, int rpt_arg, int tpc, int nring, int n_speeds, XEpi epi,
-           int napply, int mom, int rho) {
+           int napply, int mom, int rho, XRowMap rm) {
   constexpr int NL = OV * OV, NLOC = NL * OV;
   constexpr int XM = 2 * OX * OX;
   const int rpt = RPT > 0 ? RPT : rpt_arg;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long full[4];
-  const int row_len = n_xc * OX;
+  const int row_len = n_xc * OX;        // output row (local cells)
+  const int src_len = rm.src_len;       // staged source row
   const int tid = threadIdx.x;
   const int tt = tid / n_xc;                 // tile within the group
   const int cx = tid - tt * n_xc;            // x cell
@@ -52,7 +65,7 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
   // tile and group indices fit in 32 bits (the host checks n_tiles < 2^31)
   const int n_tiles = (int)((n_rows / NLOC) * per_cell);
   const int n_groups = (n_tiles + tpc - 1) / tpc;
-  const int slot_dbl = tpc * rpt * row_len;
+  const int slot_dbl = tpc * rpt * src_len;
   double* ring = sm;
   double* mid = ring + (long long)nring * slot_dbl;
   double* meta = mid + slot_dbl;             // [nring][tpc][rpt][3]: w, w*v0, w*v2
@@ -64,7 +77,9 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     const int g = k / XM, e = k - g * XM;
     xtab[k] = X.ident[g] ? ((e < OX * OX && e % (OX + 1) == 0) ? 1.0 : 0.0) : __ldg(X.mats + k);
   }
-  for (int k = tid; k < n_speeds; k += blockDim.x) xnsm[k] = X.ident[k] ? 0 : __ldg(X.nsm + k);
+  // periodic rows: the shift mod n_xc; slabs: the true shift (the halo covers it)
+  for (int k = tid; k < n_speeds; k += blockDim.x)
+    xnsm[k] = X.ident[k] ? 0 : (rm.wrap ? __ldg(X.nsm + k) : (int)__ldg(X.ns + k));
 
   // tile id -> first row and row stride (rows u = 0..rpt-1 are row0 + u*OV)
   auto tile_row0 = [&](int tile) -> long long {
@@ -92,13 +107,13 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     const int t_first = (g0 + i * gs) * tpc;
     const int nt = min(tpc, n_tiles - t_first);
     if (tid < 32) {
-      if (tid == 0) mbar_expect_tx(&full[s], (unsigned)(nt * rpt * row_len * 8));
+      if (tid == 0) mbar_expect_tx(&full[s], (unsigned)(nt * rpt * src_len * 8));
       __syncwarp();
       for (int q = tid; q < nt * rpt; q += 32) {
         const int ti = q / rpt, u = q - ti * rpt;
         const long long row = tile_row0(t_first + ti) + (long long)u * OV;
-        bulk_g2s(ring + (long long)s * slot_dbl + (ti * rpt + u) * row_len, fin + row * ld,
-                 (unsigned)(row_len * 8), &full[s]);
+        bulk_g2s(ring + (long long)s * slot_dbl + (ti * rpt + u) * src_len, fin + row * ld,
+                 (unsigned)(src_len * 8), &full[s]);
       }
     } else if (tid < 64 && need_meta) {
       for (int q = tid - 32; q < nt * rpt; q += 32) {
@@ -145,10 +160,16 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
         xa[k] = AB[k];
         xb[k] = AB[OX * OX + k];
       }
-      int a = cx - xnsm[g];   // nsm in [0, n_xc): the periodic source cell of cx
-      if (a < 0) a += n_xc;
-      ia = a * OX;
-      ib = (a == 0 ? n_xc - 1 : a - 1) * OX;
+      if (rm.wrap) {
+        int a = cx - xnsm[g];   // nsm in [0, n_xc): the periodic source cell of cx
+        if (a < 0) a += n_xc;
+        ia = a * OX;
+        ib = (a == 0 ? n_xc - 1 : a - 1) * OX;
+      } else {                  // slab: halo-relative source cells hl + cx - n, - n - 1
+        const int a = rm.hl + cx - xnsm[g];
+        ia = rm.src_off + a * OX;
+        ib = ia - OX;
+      }
     }
     auto xapply = [&](const double* srow, double* y) {
       double ua[OX], ub[OX];
@@ -169,17 +190,17 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
         y[k] = sa + sb;
       }
     };
-    const double* src = ring + (long long)s * slot_dbl + tt * rpt * row_len;
+    const double* src = ring + (long long)s * slot_dbl + tt * rpt * src_len;
     const double* mt = meta + ((long long)s * tpc + tt) * rpt * 3;
-    double* md = mid + tt * rpt * row_len;
+    double* md = mid + tt * rpt * src_len;   // (X.X: periodic rows only, src_len == row_len)
     if (napply == 2) {
       if (live) {
 #pragma unroll(RPT > 0 ? RPT : 1)
         for (int u = 0; u < rpt; ++u) {
           double y[OX];
-          xapply(src + u * row_len, y);
+          xapply(src + u * src_len, y);
 #pragma unroll
-          for (int k = 0; k < OX; ++k) md[u * row_len + cx * OX + k] = y[k];
+          for (int k = 0; k < OX; ++k) md[u * src_len + cx * OX + k] = y[k];
           if (mom) {
             const double w = mt[u * 3], wv0 = w * mt[u * 3 + 1], wv2 = w * mt[u * 3 + 2];
 #pragma unroll
@@ -198,8 +219,8 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
 #pragma unroll(RPT > 0 ? RPT : 1)
       for (int u = 0; u < rpt; ++u) {
         double y[OX];
-        xapply(src + u * row_len, y);
-        double* dst = fout + (row0 + (long long)u * OV) * ld + cx * OX;
+        xapply(src + u * src_len, y);
+        double* dst = fout + (row0 + (long long)u * OV) * rm.ld_out + rm.out_off + cx * OX;
         const double w = need_meta ? mt[u * 3] : 0.0;
         const double wv0 = (mom && napply == 1) ? w * mt[u * 3 + 1] : 0.0;
         const double wv2 = (mom && napply == 1) ? w * mt[u * 3 + 2] : 0.0;

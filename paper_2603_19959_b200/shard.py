@@ -214,6 +214,8 @@ class ShardedSimulation:
         self.width = self.lw + self.n_local * o + self.rw
         # x plan over the full periodic grid (shifts and matrices are per speed)
         self.x_plan = precompute_x_matrices(self.xgrid, self.vcoords[:, 0], 0.5 * c.dt)
+        if c.dim == 3:
+            self.x_plan.velocity_order = c.degree + 1   # enables the row-tile slab kernel
         self.poisson = PoissonSolver(self.xgrid)
         dev = device()
         self._vw = to_device_f64(self.vweights)
@@ -262,12 +264,47 @@ class ShardedSimulation:
             current_stream()), ValueError)
         self._F, self._G = self._G, self._F
 
-    def _field(self, e_out):
-        from .xfield import rho_into
-        rho_into(self.f, self._vw, self._rho_loc)
+    def _x_tiles(self, rho_out=None, mom_out3=None):
+        """Half x-step of the slab with the row-tile kernel, rho of the result (local
+        columns) or the moments of the result fused in; False if the kernel does not
+        cover this slab (then nothing was done)."""
+        import ctypes as C
+
+        from . import _capi
+        from ._device import SCRATCH, current_stream
+        if getattr(self, "_tiles_ok", None) is False:
+            return False
+        o, hl = self.o, self.halo.hl
+        lib = _capi.lib()
+        if getattr(self, "_tiles_ok", None) is None:
+            nb = C.c_size_t()
+            self._tiles_ok = lib.sldg_advect_x_slab_tiles_scratch(
+                self.x_plan.device_handle(), self.n_local, self._F.stride(0), C.byref(nb)) == 0 \
+                and self._F.stride(0) % 2 == 0
+            self._tiles_bytes = nb.value
+            if not self._tiles_ok:
+                return False
+        self.halo.exchange(self._F)
+        scratch = SCRATCH.get(("xslab", id(self)), self._tiles_bytes)
+        _capi.check(lib.sldg_advect_x_slab_tiles(
+            self.x_plan.device_handle(), self._F.data_ptr(), self._F.stride(0),
+            self.lw - hl * o, hl, self.n_local, self._G.data_ptr(), self._G.stride(0), self.lw,
+            self._vw.data_ptr(), self._v0.data_ptr(), self._v2.data_ptr(), self._xw.data_ptr(),
+            None if mom_out3 is None else mom_out3.data_ptr(),
+            None if rho_out is None else rho_out.data_ptr(), scratch.data_ptr(),
+            current_stream()), ValueError)
+        self._F, self._G = self._G, self._F
+        return True
+
+    def _solve_from_local_rho(self, e_out):
         rho = allgather_segments(self._rho_loc, [n * self.o for n in self.part.counts()],
                                  self.group)
         self.poisson.solve_into(rho.contiguous(), self._phi, e_out)
+
+    def _field(self, e_out):
+        from .xfield import rho_into
+        rho_into(self.f, self._vw, self._rho_loc)
+        self._solve_from_local_rho(e_out)
 
     def _advect_v(self, e):
         from .vsweep import advect_velocity_into
@@ -285,27 +322,35 @@ class ShardedSimulation:
         _moments_into(self.f, self._vw, self._v0, self._v2, self._xw, rec5[2:5])
         rec5[2:5] = sum_in_rank_order(rec5[2:5].clone(), self.group)
 
-    def enqueue_step(self, e_buf, rec5):
-        self._advect_x()
-        self._field(e_buf)
+    def enqueue_step(self, e_buf, rec5, v_event=None):
+        """One Strang step: 3 passes over the slab when the row-tile slab kernel covers
+        it (x + rho, v, x + moments), else x, rho, v, x, moments."""
+        import torch
+
+        from .xfield import field_diag_into
+        if self._x_tiles(rho_out=self._rho_loc):
+            self._solve_from_local_rho(e_buf)
+        else:
+            self._advect_x()
+            self._field(e_buf)
+        if v_event is not None:
+            v_event[0].record(torch.cuda.current_stream())
         self._advect_v(e_buf)
-        self._advect_x()
-        self._diag_into(e_buf, rec5)
+        if v_event is not None:
+            v_event[1].record(torch.cuda.current_stream())
+        if self._x_tiles(mom_out3=rec5[2:5]):
+            rec5[2:5] = sum_in_rank_order(rec5[2:5].clone(), self.group)
+            field_diag_into(self.poisson, e_buf, rec5[0:2])
+        else:
+            self._advect_x()
+            self._diag_into(e_buf, rec5)
 
     def advance(self, n_steps, table=None, v_events=None):
         import torch
         if table is None:
             table = torch.empty((n_steps, 5), dtype=torch.float64, device=self._F.device)
         for k in range(n_steps):
-            self._advect_x()
-            self._field(self._e)
-            if v_events is not None:
-                v_events[k][0].record(torch.cuda.current_stream())
-            self._advect_v(self._e)
-            if v_events is not None:
-                v_events[k][1].record(torch.cuda.current_stream())
-            self._advect_x()
-            self._diag_into(self._e, table[k])
+            self.enqueue_step(self._e, table[k], None if v_events is None else v_events[k])
         return table
 
     def step(self):

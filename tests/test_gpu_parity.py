@@ -491,3 +491,48 @@ def test_fused_step_any_shift_matches_separate_passes(bc, emax):
                                atol=1e-12 * abs(float(out_b[0])))
     np.testing.assert_allclose(a._rho.cpu().numpy(), b._rho.cpu().numpy(), rtol=1e-12,
                                atol=1e-12 * float(b._rho.abs().max()))
+
+
+@pytest.mark.parametrize("p,nx", [(2, 32), (1, 24)])
+def test_slab_tiles_kernel_matches_periodic(p, nx):
+    """Row-tile slab kernel (whole padded rows staged, halo-relative sources) == the
+    periodic update on the slab's columns, bitwise; its rho epilogue == rho of them."""
+    import ctypes as C
+
+    from paper_2603_19959_b200 import _capi, shard
+    from paper_2603_19959_b200._device import current_stream
+    from paper_2603_19959_b200.xfield import advect_x_into
+    cfg = sv.SimConfig(dim=3, n_base=4, levels=1, degree=p, n_x=nx, degree_x=2, n_steps=1)
+    sim = sv.Simulation(cfg)
+    o = sim.xgrid.degree + 1
+    rng = np.random.default_rng(nx + p)
+    fg = rng.standard_normal(tuple(sim.f.shape))
+    full = torch.empty_like(sim.f)
+    advect_x_into(dev(fg), full, sim.x_plan)
+    sp = sim.vcoords[:, 0]
+    hl, hr = shard.x_halo_cells(sim.xgrid.h, sp, 0.5 * cfg.dt)
+    w = dev(sim.vweights)
+    for c0, nl in ((0, 8), (8, 8), (nx - 8, 8), (3, 10)):
+        lw, rw = shard.margin_dofs(hl, o), shard.margin_dofs(hr, o)
+        width = lw + nl * o + rw
+        width += width & 1
+        ext = np.zeros((fg.shape[0], width))
+        cells = [(c0 - hl + k) % nx for k in range(hl + nl + hr)]
+        blk = np.concatenate([fg[:, c * o:(c + 1) * o] for c in cells], axis=1)
+        ext[:, lw - hl * o:lw + (nl + hr) * o] = blk
+        e_d = dev(ext)
+        out = torch.zeros_like(e_d)
+        nb = C.c_size_t()
+        _capi.check(_capi.lib().sldg_advect_x_slab_tiles_scratch(
+            sim.x_plan.device_handle(), nl, width, C.byref(nb)))
+        scr = torch.empty(nb.value, dtype=torch.uint8, device=DEV)
+        rho = torch.empty(nl * o, dtype=torch.float64, device=DEV)
+        _capi.check(_capi.lib().sldg_advect_x_slab_tiles(
+            sim.x_plan.device_handle(), e_d.data_ptr(), width, lw - hl * o, hl, nl,
+            out.data_ptr(), width, lw, w.data_ptr(), None, None, None, None, rho.data_ptr(),
+            scr.data_ptr(), current_stream()))
+        got = out[:, lw:lw + nl * o].cpu().numpy()
+        ref = full[:, c0 * o:(c0 + nl) * o].cpu().numpy()
+        assert np.array_equal(got, ref), (c0, nl)
+        r_ref = sim.vweights @ ref
+        assert np.abs(rho.cpu().numpy() - r_ref).max() <= 1e-13 * np.abs(r_ref).max()
