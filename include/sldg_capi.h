@@ -230,6 +230,10 @@ int sldg_field_diag(const sldg_poisson* p, const double* e, double* out2, void* 
  * _query returns SLDG_ERR_UNSUPPORTED (with the reason) for plans it does not cover. */
 int sldg_step_fused_query(const sldg_vplan* vplan, const sldg_xplan* xplan, int64_t n_cols,
                           int64_t ld, size_t* scratch_bytes);
+/* *profitable = 1 when the one-pass step is expected to beat the separate passes on
+ * this device (its kernel keeps two CTAs per SM without register spills). */
+int sldg_step_fused_advice(const sldg_vplan* vplan, const sldg_xplan* xplan, int64_t n_cols,
+                           int64_t ld, int32_t* profitable);
 int sldg_step_fused(const sldg_vplan* vplan, const sldg_xplan* xplan, const double* f_in,
                     double* f_out, int64_t ld, int64_t n_cols, const double* speeds, double dt,
                     int32_t bc, const double* w, const double* v0, const double* v2,

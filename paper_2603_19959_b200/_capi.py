@@ -71,6 +71,8 @@ _SIGS = {
     "sldg_launch_count": (C.c_int64, []),
     "sldg_step_fused_query": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                         C.POINTER(C.c_size_t)]),
+    "sldg_step_fused_advice": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                         C.POINTER(C.c_int32)]),
     "sldg_step_fused": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                   C.c_int64, C.c_void_p, C.c_double, C.c_int32, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -910,6 +910,32 @@ int sldg_step_fused_query(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_
   return SLDG_OK;
 }
 
+int sldg_step_fused_advice(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_cols, int64_t ld,
+                           int32_t* profitable) {
+  if (!vp || !xp || !profitable) {
+    set_error("null argument");
+    return SLDG_ERR_ARG;
+  }
+  FusedGeom g;
+  int rc = check_geom(vp, xp, n_cols, ld, &g);
+  if (rc) return rc;
+  FusedKernel k = fused_kernel(vp, xp, g);
+  if (!k) {
+    set_error("fused step: no kernel for this degree / line group");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  // measured: the one-pass step beats the separate passes when its
+  // kernel keeps two CTAs per SM without register spills; otherwise (wide rows,
+  // degree-3 velocity or x bases) the separate passes are as fast or faster
+  cudaFuncAttributes attr;
+  SLDG_CUDA_TRY(cudaFuncGetAttributes(&attr, k));
+  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  int per_sm = 0;
+  SLDG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, g.threads, g.smem));
+  *profitable = (attr.localSizeBytes == 0 && per_sm >= 2) ? 1 : 0;
+  return SLDG_OK;
+}
+
 int sldg_step_fused(const sldg_vplan* vp, const sldg_xplan* xp, const double* fin, double* fout,
                     int64_t ld, int64_t n_cols, const double* speeds, double dt, int32_t bc,
                     const double* w, const double* v0, const double* v2, const double* xw,

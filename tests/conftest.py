@@ -10,6 +10,10 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# the parity tests exercise the one-pass fused step wherever it is supported, not
+# only where the library advises it (Simulation.fused_policy)
+os.environ.setdefault("SLDG_FUSED", "force")
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")

@@ -536,3 +536,32 @@ def test_slab_tiles_kernel_matches_periodic(p, nx):
         assert np.array_equal(got, ref), (c0, nl)
         r_ref = sim.vweights @ ref
         assert np.abs(rho.cpu().numpy() - r_ref).max() <= 1e-13 * np.abs(r_ref).max()
+
+
+def test_fused_step_advice():
+    """The library advises the one-pass step for the headline shape (two CTAs per SM, no
+    spills) and not for shapes whose kernel spills or runs one CTA per SM; the default
+    policy follows the advice, "force" / "off" override it."""
+    import ctypes as C
+
+    from paper_2603_19959_b200 import _capi
+
+    def advice(**kw):
+        s = sv.Simulation(sv.SimConfig(**kw, n_steps=1))
+        adv = C.c_int32(-1)
+        _capi.check(_capi.lib().sldg_step_fused_advice(
+            s.sweep_plan.device_handle(), s.x_plan.device_handle(), s.f.shape[1],
+            s.f.stride(0), C.byref(adv)))
+        return adv.value, s
+
+    yes, s = advice(dim=3, n_base=4, levels=0, degree=2, n_x=64)
+    assert yes == 1
+    s.fused_policy = "auto"
+    assert s.fused_step_supported()
+    no, s = advice(dim=3, n_base=4, levels=0, degree=2, n_x=64, degree_x=3)
+    assert no == 0
+    s.fused_policy = "auto"
+    assert not s.fused_step_supported()
+    s2 = sv.Simulation(sv.SimConfig(dim=3, n_base=4, levels=0, degree=2, n_x=64, n_steps=1))
+    s2.fused_policy = "off"
+    assert not s2.fused_step_supported()
