@@ -251,8 +251,11 @@ int sldg_step_fused(const sldg_vplan* vplan, const sldg_xplan* xplan, const doub
  * mode 1 = the last step of a run: f_out = X(V(f_in)), the state after the full
  * step (no next leading half step, no rho); mode 2 = the first (leading) half
  * x-step alone, f_out = X(f_in) with rho partials (speeds unused) -- the same tile
- * distribution, for pencil sharding.  Results are bitwise identical to the
- * separate calls (mode 2: rho in a different summation order). */
+ * distribution, for pencil sharding.  Modes 1 and 2 give the separate calls' f
+ * bit for bit; mode 0 applies the two half x-steps as one composed stencil
+ * (A A, A B + B A, B B), equal to the separate calls to ~1e-16 relative.  The
+ * x weights `xw` are the x DOF weights of the plan's uniform grid (every cell's
+ * weights equal cell 0's, xfield.py XGrid.dof_weights). */
 int sldg_field_chain(const sldg_vplan* vplan, const sldg_xplan* xplan, const sldg_poisson* p,
                      int64_t n_cols, int64_t ld, double dt, const double* rho_in, double* rho,
                      double* phi, double* e, double* diag2, double* mom_prev3, void* scratch,

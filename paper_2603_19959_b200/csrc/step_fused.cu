@@ -10,13 +10,17 @@
 // R = LG*OV rows spanning all x columns) the kernel performs
 //   V  : whole-pencil fast path (sweep_pencil, vsweep.py:197-200) from a TMA
 //        bulk-copy ring of cell tiles (as k_sweep_stream), into shared memory;
-//   X1 : trailing half x-step on the tile's rows (they are complete rows),
-//        moments of the result accumulated;
-//   X2 : leading half x-step of the next step, rho of the result accumulated,
+//   X  : trailing half x-step of this step and leading half x-step of the
+//        next on the tile's rows (they are complete rows), as ONE composed
+//        3-cell stencil (both half steps use the row's x-speed: X.X = C0, C1,
+//        C2 = A A, A B + B A, B B), moments of the intermediate (trailing) state
+//        through the contracted weights A^T xw, B^T xw, rho of the result;
 //        result stored to HBM.
 // Every coefficient is read once and written once per step: 16 B/DOF instead
-// of 32 B/DOF for the separate sweep and X.X passes.  Arithmetic per output is
-// the same as in k_sweep_stream / k_xadv (same operands, same order).
+// of 32 B/DOF for the separate sweep and X.X passes.  V is the same arithmetic
+// as k_sweep_stream; the composed x-step re-associates X(X(u)) (differences
+// from the separate passes ~1e-16 relative per step, far inside the 1e-12
+// parity budget; tests/test_gpu_parity.py::test_fused_step_matches_unfused_*).
 //
 // Work decomposition: persistent CTAs (resident count x SMs).  The work is the
 // sequence of items (walk pencil, line group), each a run of cell tiles; CTA b
@@ -106,6 +110,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   const int n_cols = NXC > 0 ? OX * NXC : n_cols_arg;
   const int rw = NXC > 0 ? ((OX * NXC) | 1) : rw_arg;
   constexpr int XM = 2 * OX * OX;
+  constexpr int XCS = 3 * OX * OX + 2 * OX;     // composed x-step entries per v_x node
   constexpr int R = LG * OV;                    // rows per tile
   constexpr int n_lg = OV * OV / LG;
   extern __shared__ __align__(128) double sm[];
@@ -115,12 +120,14 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
 
   const int tile = R * n_cols;                  // doubles per ring slot
   double* ring = sm;
-  double* stA = ring + kFRing * tile;
-  double* stB = stA + R * rw;
-  double* xtab = stB + R * rw;                  // n_speeds x (A|B) for the x shift
+  double* stA = ring + kFRing * tile;          // two tile buffers of R rows (stride rw)
+  double* xtab = stA + 2 * R * rw;                 // n_speeds x (A|B) for the x shift
   int* xns = reinterpret_cast<int*>(xtab + (long long)n_speeds * XM);
-  double* xws = xtab + (long long)n_speeds * XM + (n_speeds + 1) / 2;   // x quadrature weights
-  double* tabs0 = xws + n_cols;
+  // composed x-step per tile and v_x node (MODE 0), two buffers alternating like
+  // the tile buffers: C0 = A A, C1 = A B + B A, C2 = B B, then cA = A^T xw, cB = B^T xw
+  double* xcmp = xtab + (long long)n_speeds * XM + (n_speeds + 1) / 2;
+  double* xw0 = xcmp + 2 * OV * XCS;            // x quadrature weights of one cell
+  double* tabs0 = xw0 + OX;
   const int tab_dbl = nmax + 3 * R * nmax + (nmax * OV + 1) / 2;
   auto tabs = [&](int b) -> ItemTabs {
     double* base = tabs0 + (long long)b * tab_dbl;
@@ -150,7 +157,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     xtab[k] = X.ident[g] ? ((e < OX * OX && e % (OX + 1) == 0) ? 1.0 : 0.0) : __ldg(X.mats + k);
   }
   for (int k = tid; k < n_speeds; k += nthr) xns[k] = X.ident[k] ? 0 : (int)X.ns[k];
-  for (int k = tid; k < n_cols; k += nthr) xws[k] = __ldg(fa.xw + k);
+  if (tid < OX) xw0[tid] = __ldg(fa.xw + tid);   // uniform x grid: every cell's weights
   if (tid < kMaxLev) {
     s_nsmin[tid] = 1 << 30;
     s_nsmax[tid] = -(1 << 30);
@@ -186,20 +193,24 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   auto wd_lev = [&](int b) { return (int)(s_wd[b][1] >> 32); };
   // prefetch stages of item `it` into table buffer b (cp.async, completed by the
   // caller's cp_async_wait_all + __syncthreads before the next stage reads them)
+  // per-tile extra work sits on different warps: the compose on threads 0.., the
+  // ring pump on the last warp, the table stages from the second-to-last warp on
+  const int pump_tid = nthr - 32;
+  const int rt = tid >= nthr - 64 ? tid - (nthr - 64) : tid + 64;
   auto stage = [&](int st, int b, long long it) {
     const ItemTabs T = tabs(b);
     if (st == 0) {
-      if (tid == 0) cp_async16(&s_wd[b][0], P.walk_desc + 2 * item_wp(it));
+      if (rt == 0) cp_async16(&s_wd[b][0], P.walk_desc + 2 * item_wp(it));
     } else if (st == 1) {
       const long long off = s_wd[b][0];
       const int n = wd_n(b);
-      for (int k = tid; k < n; k += nthr) cp_async8(T.crow + k, P.e_row0 + off + k);
+      for (int k = rt; k < n; k += nthr) cp_async8(T.crow + k, P.e_row0 + off + k);
     } else {
       const int n = wd_n(b);
       const long long l0 = (long long)item_t0(it) * OV;
-      for (int k = tid; k < n * OV; k += nthr)
+      for (int k = rt; k < n * OV; k += nthr)
         cp_async4(T.cg + k, X.row_speed + T.crow[k / OV] + l0 + k % OV);
-      for (int k = tid; k < n * 3 * R; k += nthr) {
+      for (int k = rt; k < n * 3 * R; k += nthr) {
         const int s2 = k / (3 * R), rem = k - s2 * 3 * R, a = rem / R, r = rem - a * R;
         const double* src = a == 0 ? fa.w : (a == 1 ? fa.v0 : fa.v2);
         cp_async8(T.cm + k, src + T.crow[s2] + l0 + r);
@@ -238,10 +249,10 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   // periodic, clipped when absorbing); non-streamable items load nothing.
   auto seg_first = [&](int sb) { return per ? sb - 1 : max(sb - 1, 0); };
   auto seg_last = [&](int se, int n) { return per ? se : min(se, n - 1); };
-  // thread-0 issue cursor, kept in shared memory (no registers across the loop):
+  // pump-thread issue cursor, kept in shared memory (no registers across the loop):
   // item, next cell, last cell, loads issued, cursor initialised for the item
   __shared__ int s_cur[5];
-  if (tid == 0) {
+  if (tid == pump_tid) {
     s_cur[0] = 0;
     s_cur[1] = 0;
     s_cur[2] = -1;
@@ -290,11 +301,11 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   int base = 0;   // load index of the current item's first load
   int waited = -1;   // highest load index this thread has waited for
 
-  // V phase of one column: rows t*OV+i of the source cells sa / sb -> stA column c.
-  // CHECKED: the source cells may lie outside the pencil (absorbing ends).
-  auto vcol = [&](const double* sa, const double* sb, bool va, bool vb, auto checked) {
+  // V phase of one column: rows t*OV+i of the source cells sa / sb -> column c of
+  // the tile buffer `out`.  CHECKED: the source cells may lie outside the pencil
+  // (absorbing ends).
+  auto vcol = [&](double* out, const double* sa, const double* sb, bool va, bool vb, auto checked) {
     constexpr bool CK = decltype(checked)::value;
-    double* out = stA + c;
 #pragma unroll
     for (int t = 0; t < LG; ++t) {
       double ua[OV], ub[OV], y[OV];
@@ -314,10 +325,26 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       for (int i = 0; i < OV; ++i) out[(t * OV + i) * rw] = y[i];
     }
   };
-  auto vcopy = [&](const double* me) {
+  auto vcopy = [&](double* out, const double* me) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) stA[r * rw + c] = me[r * n_cols];
+    for (int r = 0; r < R; ++r) out[r * rw] = me[r * n_cols];
   };
+  // 1-D periodic shift of the x cells of one row by the x-speed's (A, B): cell
+  // sources ua (cell - n) and ub (cell - n - 1), same arithmetic as k_xadv
+  auto xmul = [&](const double* xa, const double* xb, const double* ua, const double* ub, double* y) {
+#pragma unroll
+    for (int k = 0; k < OX; ++k) {
+      double sa = xa[k * OX] * ua[0];
+      double sb2 = xb[k * OX] * ub[0];
+#pragma unroll
+      for (int j = 1; j < OX; ++j) {
+        sa = fma(xa[k * OX + j], ua[j], sa);
+        sb2 = fma(xb[k * OX + j], ub[j], sb2);
+      }
+      y[k] = sa + sb2;
+    }
+  };
+  auto wrap = [&](int k) { return k < 0 ? k + n_xc : (k >= n_xc ? k - n_xc : k); };
 
   for (int i = 0; i < n_items; ++i) {
     const int b = i & 1;
@@ -337,162 +364,235 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       }
     }
     const bool has_next = i + 1 < n_items;
-    int n_staged = 0;   // prefetch stages of the next item issued so far
-    for (int s = sb; s < se; ++s) {
-      const double* mcur = T.cm + (long long)s * 3 * R;
-      const long long r0 = T.crow[s] + l0;
-      const int g_cur = xv ? T.cg[s * OV + iv] : 0;
-      // ===================== V: pencil sweep of cell s -> stA (rows of R, stride rw)
+    int n_staged = 0;   // tile barriers passed in this item (= prefetch stages issued + 1)
+
+    // ===================== V: pencil sweep of cell s -> tile buffer (R rows, stride rw)
+    auto v_pump = [&](int s) {
+      if (streamable && tid == pump_tid) pump(base + max(s - 1, first) - first + kFRing, i, n_staged >= 4);
+    };
+    auto v_tile = [&](int s, double* dst) {
       if (streamable) {
         const int klo = base + max(s - 1, first) - first, khi = base + min(s + 1, last) - first;
-        if (tid == 0) pump(klo + kFRing, i, n_staged >= 4);
         // loads up to `waited` were waited for at earlier tiles (their slots are
         // not refilled before every thread is past them): only the new ones
         for (unsigned k = (unsigned)max(klo, waited + 1); k <= (unsigned)khi; ++k)
           mbar_wait(&full[k & (kFRing - 1)], (k / kFRing) & 1u);
         waited = max(waited, khi);
         if (colv) {
+          double* out = dst + c;
           auto slot = [&](int cell) { return ring + ((base + cell - first) & (kFRing - 1)) * tile + c; };
           if (speed == 0.0) {
-            vcopy(slot(s));
+            vcopy(out, slot(s));
           } else {
             // streamable: source cells s - nsv and s - nsv - 1 with nsv in {-1, 0}
             const int va_cell = s - (int)nsv, vb_cell = va_cell - 1;
             if (per || (s > 0 && s < n - 1)) {
-              vcol(slot(va_cell), slot(vb_cell), true, true, BoolC<false>{});
+              vcol(out, slot(va_cell), slot(vb_cell), true, true, BoolC<false>{});
             } else {
               const bool va = va_cell >= 0 && va_cell < n, vb = vb_cell >= 0 && vb_cell < n;
-              vcol(slot(va ? va_cell : s), slot(vb ? vb_cell : s), va, vb, BoolC<true>{});
+              vcol(out, slot(va ? va_cell : s), slot(vb ? vb_cell : s), va, vb, BoolC<true>{});
             }
           }
         }
-      } else {
-        if (colv) {
-          if (speed == 0.0) {
-            vcopy(fin + r0 * n_cols + c);
+      } else if (colv) {
+        double* out = dst + c;
+        const long long r0 = T.crow[s] + l0;
+        if (speed == 0.0) {
+          vcopy(out, fin + r0 * n_cols + c);
+        } else {
+          long long qa = s - nsv, qb = s - nsv - 1;
+          bool va = true, vb = true;
+          if (per) {
+            qa = pymod(qa, n);
+            qb = pymod(qb, n);
           } else {
-            long long qa = s - nsv, qb = s - nsv - 1;
-            bool va = true, vb = true;
-            if (per) {
-              qa = pymod(qa, n);
-              qb = pymod(qb, n);
-            } else {
-              va = qa >= 0 && qa < n;
-              vb = qb >= 0 && qb < n;
-            }
-            vcol(fin + (T.crow[va ? (int)qa : s] + l0) * n_cols + c,
-                 fin + (T.crow[vb ? (int)qb : s] + l0) * n_cols + c, va, vb, BoolC<true>{});
+            va = qa >= 0 && qa < n;
+            vb = qb >= 0 && qb < n;
           }
+          vcol(out, fin + (T.crow[va ? (int)qa : s] + l0) * n_cols + c,
+               fin + (T.crow[vb ? (int)qb : s] + l0) * n_cols + c, va, vb, BoolC<true>{});
         }
       }
-      // x shift of this thread's rows for cell s: matrices to registers, wrapped sources
+    };
+    // ===================== X of cell s from its V result `src`:
+    //   MODE 0: trailing half step X1 (+ moments) and the next step's leading half
+    //     step X2 (+ rho) -> HBM.  Both use the row's x-speed, so X2 at cell cx
+    //     depends on the V result at cells a - n, a - n - 1, a - n - 2 (a = cx - n)
+    //     through the composed matrices; the moments take X1 at cell a (cx -> a is a
+    //     bijection of the row's cells).
+    //   MODE 1: X1 (+ moments) -> HBM;  MODE 2: X1 (+ rho) -> HBM.
+    auto x_tile = [&](int s, const double* src, const double* src_cmp) {
+      if (!xv) return;
+      const double* mcur = T.cm + (long long)s * 3 * R;
+      const long long r0 = T.crow[s] + l0;
+      const int g = T.cg[s * OV + iv];
       double xa[OX * OX], xb[OX * OX];
-      int ia = 0, ib = 0;
-      if (xv) {
-        const double* AB = xtab + (long long)g_cur * XM;
+      const double* AB = xtab + (long long)g * XM;
 #pragma unroll
-        for (int k = 0; k < OX * OX; ++k) {
-          xa[k] = AB[k];
-          xb[k] = AB[OX * OX + k];
-        }
-        ia = cx - xns[g_cur];
-        ia = ia < 0 ? ia + n_xc : (ia >= n_xc ? ia - n_xc : ia);
-        ib = ia == 0 ? n_xc - 1 : ia - 1;
-        ia *= OX;
-        ib *= OX;
+      for (int k = 0; k < OX * OX; ++k) {
+        xa[k] = AB[k];
+        xb[k] = AB[OX * OX + k];
       }
-      auto xapply = [&](const double* srow, double* y) {
-        double ua[OX], ub[OX];
+      const int ns = xns[g];
+      const int ca = wrap(cx - ns);
+      double* dst = fout + (r0 + iv) * n_cols + cx * OX;
+      if (MODE == 0) {
+        // composed step: y = C0 u(a - n) + C1 u(a - n - 1) + C2 u(a - n - 2), a = cx - n,
+        // one matrix at a time over the tile's LG rows (each matrix's partial sums
+        // are formed separately and added in the order (s0 + s1) + s2); the trailing
+        // half step's moment weight is z = xw . X1(a) = cA . u0 + cB . u1
+        const double* Cc = src_cmp + iv * XCS;
+        const int p0 = wrap(ca - ns);
+        const int p1 = p0 == 0 ? n_xc - 1 : p0 - 1;
+        const int p2 = p1 == 0 ? n_xc - 1 : p1 - 1;
+        double acc[LG][OX], zs[LG];
 #pragma unroll
-        for (int j = 0; j < OX; ++j) {
-          ua[j] = srow[ia + j];
-          ub[j] = srow[ib + j];
-        }
+        for (int m = 0; m < 3; ++m) {
+          double cm[OX * OX], cz[OX];
 #pragma unroll
-        for (int k = 0; k < OX; ++k) {
-          double sa = xa[k * OX] * ua[0];
-          double sb2 = xb[k * OX] * ub[0];
+          for (int k = 0; k < OX * OX; ++k) cm[k] = Cc[m * OX * OX + k];
+          if (m < 2) {
 #pragma unroll
-          for (int j = 1; j < OX; ++j) {
-            sa = fma(xa[k * OX + j], ua[j], sa);
-            sb2 = fma(xb[k * OX + j], ub[j], sb2);
+            for (int k = 0; k < OX; ++k) cz[k] = Cc[3 * OX * OX + m * OX + k];
           }
-          y[k] = sa + sb2;
+          const int pc = (m == 0 ? p0 : (m == 1 ? p1 : p2)) * OX;
+#pragma unroll
+          for (int t = 0; t < LG; ++t) {
+            const double* u = src + (t * OV + iv) * rw + pc;
+            double uu[OX];
+#pragma unroll
+            for (int j = 0; j < OX; ++j) uu[j] = u[j];
+#pragma unroll
+            for (int k = 0; k < OX; ++k) {
+              double sm_ = cm[k * OX] * uu[0];
+#pragma unroll
+              for (int j = 1; j < OX; ++j) sm_ = fma(cm[k * OX + j], uu[j], sm_);
+              acc[t][k] = m == 0 ? sm_ : acc[t][k] + sm_;
+            }
+            if (m < 2) {
+              double zz = cz[0] * uu[0];
+#pragma unroll
+              for (int j = 1; j < OX; ++j) zz = fma(cz[j], uu[j], zz);
+              zs[t] = m == 0 ? zz : zs[t] + zz;
+            }
+          }
         }
-      };
-      // prefetch stage copies issued at the previous step complete before this barrier
-      if (n_staged > 0 && n_staged <= 3) cp_async_wait_all();
-      __syncthreads();
-      if (has_next && n_staged < 3) stage(n_staged, b ^ 1, it + 1);
-      ++n_staged;
-      // ===================== X1 (trailing half step): stA -> stB (or HBM for the
-      // last step of a run), moments; lead mode: the half step of the first step,
-      // -> HBM, rho
-      if (xv) {
 #pragma unroll
         for (int t = 0; t < LG; ++t) {
           const int r = t * OV + iv;
-          double y[OX];
-          xapply(stA + r * rw, y);
           const double wr = mcur[r];
-          double z = 0.0, wv0 = 0.0, wv2 = 0.0;
-          if (MODE != 2) {
-            wv0 = wr * mcur[R + r];
-            wv2 = wr * mcur[2 * R + r];
-            z = xws[cx * OX] * y[0];
+          const double wv0 = wr * mcur[R + r], wv2 = wr * mcur[2 * R + r];
 #pragma unroll
-            for (int k = 1; k < OX; ++k) z = fma(xws[cx * OX + k], y[k], z);
+          for (int k = 0; k < OX; ++k) {
+            dst[k] = acc[t][k];
+            rha[k] = fma(wr, acc[t][k], rha[k]);
           }
-          if (MODE != 0) {
-            double* o = fout + (r0 + r) * n_cols + cx * OX;
+          m0 = fma(wr, zs[t], m0);
+          m1 = fma(wv0, zs[t], m1);
+          m2 = fma(wv2, zs[t], m2);
+          dst += (long long)OV * n_cols;
+        }
+      } else {
+        const int ia = ca * OX, ib = (ca == 0 ? n_xc - 1 : ca - 1) * OX;
 #pragma unroll
-            for (int k = 0; k < OX; ++k) o[k] = y[k];
-          } else {
-            double* o = stB + r * rw + cx * OX;
+        for (int t = 0; t < LG; ++t) {
+          const int r = t * OV + iv;
+          const double* srow = src + r * rw;
+          double ua[OX], ub[OX], y[OX];
 #pragma unroll
-            for (int k = 0; k < OX; ++k) o[k] = y[k];
+          for (int j = 0; j < OX; ++j) {
+            ua[j] = srow[ia + j];
+            ub[j] = srow[ib + j];
           }
+          xmul(xa, xb, ua, ub, y);
+          const double wr = mcur[r];
+#pragma unroll
+          for (int k = 0; k < OX; ++k) dst[k] = y[k];
           if (MODE == 2) {
 #pragma unroll
             for (int k = 0; k < OX; ++k) rha[k] = fma(wr, y[k], rha[k]);
           } else {
+            const double wv0 = wr * mcur[R + r], wv2 = wr * mcur[2 * R + r];
+            double z = xw0[0] * y[0];
+#pragma unroll
+            for (int k = 1; k < OX; ++k) z = fma(xw0[k], y[k], z);
             m0 = fma(wr, z, m0);
             m1 = fma(wv0, z, m1);
             m2 = fma(wv2, z, m2);
           }
-        }
-      }
-      __syncthreads();
-      // ===================== X2 (next step's leading half): stB -> HBM, rho
-      // No barrier after X2: the next V writes stA (last read in X1, before the
-      // barrier above) and the ring slot it refills was last read in this V.
-      if (xv && MODE == 0) {
-        double* dst = fout + (r0 + iv) * n_cols + cx * OX;
-#pragma unroll
-        for (int t = 0; t < LG; ++t) {
-          const int r = t * OV + iv;
-          double y[OX];
-          xapply(stB + r * rw, y);
-          const double wr = mcur[r];
-#pragma unroll
-          for (int k = 0; k < OX; ++k) {
-            dst[k] = y[k];
-            rha[k] = fma(wr, y[k], rha[k]);
-          }
           dst += (long long)OV * n_cols;
         }
       }
+    };
+    // MODE 0: composed x-step of cell s's v_x nodes -> dst (XCS entries per node)
+    auto x_compose = [&](int s, double* dst) {
+      if (MODE != 0) return;
+      for (int e0 = tid; e0 < OV * XCS; e0 += nthr) {   // the CTA may have < OV*XCS threads
+        const int jv = e0 / XCS, e = e0 - jv * XCS;
+        const double* A = xtab + (long long)T.cg[s * OV + jv] * XM;
+        const double* B = A + OX * OX;
+        double v;
+        if (e < 3 * OX * OX) {
+          const int w = e / (OX * OX), k = (e / OX) % OX, j = e % OX;
+          const double* L = w == 2 ? B : A;
+          const double* Rm = w == 0 ? A : B;
+          v = L[k * OX] * Rm[j];
+#pragma unroll
+          for (int m = 1; m < OX; ++m) v = fma(L[k * OX + m], Rm[m * OX + j], v);
+          if (w == 1) {
+#pragma unroll
+            for (int m = 0; m < OX; ++m) v = fma(B[k * OX + m], A[m * OX + j], v);
+          }
+        } else {
+          const int q = e - 3 * OX * OX, j = q % OX;
+          const double* M = q < OX ? A : B;
+          v = xw0[0] * M[j];
+#pragma unroll
+          for (int k = 1; k < OX; ++k) v = fma(xw0[k], M[k * OX + j], v);
+        }
+        dst[e0] = v;
+      }
+    };
+    // one CTA barrier per tile; the next item's table prefetch advances one stage
+    // per barrier (copies issued after barrier k complete before barrier k + 1)
+    auto tile_barrier = [&]() {
+      if (n_staged > 0 && n_staged <= 3) cp_async_wait_all();
+      __syncthreads();
+      if (has_next && n_staged < 3) stage(n_staged, b ^ 1, it + 1);
+      ++n_staged;
+    };
+
+    // software pipeline over the item's cells, tile buffers alternating: V(s+1)
+    // and X(s) between the same two barriers (X(s) reads the buffer V(s) wrote
+    // before the previous barrier; V(s+1) writes the buffer X(s-1) read before it;
+    // the ring slot a pump refills was last read by a V before the previous barrier)
+    v_pump(sb);
+    x_compose(sb, xcmp);
+    v_tile(sb, stA);
+    tile_barrier();
+    for (int s = sb; s < se; ++s) {
+      const int j = s - sb;
+      double* cur = stA + (j & 1) * R * rw;
+      double* nxt = stA + ((j + 1) & 1) * R * rw;
+      if (s + 1 < se) v_pump(s + 1);
+      x_tile(s, cur, xcmp + (j & 1) * OV * XCS);
+      if (s + 1 < se) {
+        x_compose(s + 1, xcmp + ((j + 1) & 1) * OV * XCS);
+        v_tile(s + 1, nxt);
+      }
+      tile_barrier();
     }
     if (streamable && se > sb) base += last - first + 1;
-    if (has_next) {
+    if (has_next && n_staged < 4) {
       // finish the next item's prefetch when this segment was too short to hide it
-      if (n_staged >= 1 && n_staged <= 3) cp_async_wait_all();
-      __syncthreads();   // also: the next item overwrites nothing this one still reads
-      for (int st = max(n_staged, 0); st < 3; ++st) stage_sync(st, b ^ 1, it + 1);
+      if (n_staged >= 1) cp_async_wait_all();
+      __syncthreads();
+      for (int st = n_staged; st < 3; ++st) stage_sync(st, b ^ 1, it + 1);
     }
   }
   grid_dep_launch();   // the next field chain may be scheduled (it waits for our end)
-  __syncthreads();     // stB (read by X2) is reused by the reduction below
+  // (the tile buffers are reused by the reduction below: the last tile barrier
+  // separates it from the last X)
 
   // ---- CTA partials: rho per column (over i_v in order), moments contracted with xw
   double* red = stA;   // reuse: OV x n_cols, then 3 x blockDim
@@ -559,7 +659,7 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   g.rw = (int)n_cols + (n_cols % 2 == 0 ? 1 : 0);   // odd row stride: conflict-free columns
   g.nmax = vp->max_walk_cells;
   const size_t fixed = sizeof(double) * (size_t)xp->n_speeds * 2 * OX * OX +
-                       sizeof(double) * ((xp->n_speeds + 1) / 2 + n_cols) + 64;
+                       sizeof(double) * ((xp->n_speeds + 1) / 2 + 2 * OV * (3 * OX * OX + 2 * OX) + OX) + 64;
   const size_t nmax = (size_t)g.nmax;
   const size_t budget = 227 * 1024 - 1024;
   g.lg = 0;
