@@ -55,7 +55,7 @@ static __global__ void k_fold_cols(const double* __restrict__ part, long long n_
   const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
   if (c >= n_cols) return;
   double s = 0.0;
-  for (long long k = lane; k < n_parts; k += 32) s += part[k * n_cols + c];
+  for (long long k = lane; k < n_parts; k += 32) s += part[c * n_parts + k];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) out[c] = s;
@@ -80,7 +80,7 @@ struct FusedArgs {
   const double* v2;
   const double* xw;
   double* mom_part;   // [grid][3]
-  double* rho_part;   // [grid][n_cols]
+  double* rho_part;   // [n_cols][grid] (column-major: a column's partials are contiguous)
 };
 
 template <bool B>
@@ -143,7 +143,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   const long long te = t_begin + (long long)(blockIdx.x + 1) * n_tiles / gridDim.x;
   if (te <= tb) {   // empty share: zero partials keep the folds over the grid valid
     grid_dep_wait();   // the preceding field chain may still be folding the partials
-    for (int k = tid; k < n_cols_arg; k += nthr) fa.rho_part[(long long)blockIdx.x * n_cols_arg + k] = 0.0;
+    for (int k = tid; k < n_cols_arg; k += nthr) fa.rho_part[(long long)k * gridDim.x + blockIdx.x] = 0.0;
     if (tid < 3) fa.mom_part[blockIdx.x * 3 + tid] = 0.0;
     return;
   }
@@ -604,7 +604,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   if (colv) {
     double s = 0.0;
     for (int k = 0; k < OV; ++k) s += red[k * n_cols + c];
-    fa.rho_part[(long long)blockIdx.x * n_cols + c] = s;
+    fa.rho_part[(long long)c * gridDim.x + blockIdx.x] = s;
   }
   __syncthreads();
   red[tid] = m0;
@@ -798,7 +798,7 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
               DevBasis vb, double dt, double base_width, int n_levels,
               long long* __restrict__ lm_ns, double* __restrict__ lm_frac,
               double* __restrict__ lm_mats) {
-  constexpr int CH = 80;   // columns per fold chunk
+  constexpr int CH = 80;   // fsm: 32 x (CH + 1) doubles, b of the GEMV when it fits
   __shared__ double red[1024], red2[1024];
   __shared__ double fsm[32 * (CH + 1)];
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, nw = blockDim.x >> 5;
@@ -812,27 +812,16 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
   const double* r = rho_in;
   if (!r) {
     // fold the previous fused step's partials in k_fold_cols' order (lane l sums
-    // parts l, l+32, ...; then the xor butterfly), with coalesced loads: thread
-    // (l, column) forms lane l's sum, a warp per column does the butterfly
-    for (int c0 = 0; c0 < nd; c0 += CH) {
-      const int nc = min(CH, nd - c0);
-      for (int idx = tid; idx < 32 * nc; idx += blockDim.x) {
-        const int l = idx / nc, cc = idx - l * nc;
-        const double* q = rho_part + (size_t)l * nd + c0 + cc;
-        const size_t stride = (size_t)32 * nd;
-        double s = 0.0;
+    // parts l, l+32, ...; then the xor butterfly): a warp per column, its partials
+    // contiguous (column-major), every warp's loads in flight at once
+    for (int c = wp; c < nd; c += nw) {
+      const double* q = rho_part + (size_t)c * np;
+      double s = 0.0;
 #pragma unroll 4
-        for (int k = l; k < np; k += 32, q += stride) s += __ldg(q);
-        fsm[l * (CH + 1) + cc] = s;
-      }
-      __syncthreads();
-      for (int cc = wp; cc < nc; cc += nw) {
-        double s = fsm[lane * (CH + 1) + cc];
+      for (int k = lane; k < np; k += 32) s += __ldg(q + k);
 #pragma unroll
-        for (int of = 16; of > 0; of >>= 1) s += __shfl_xor_sync(0xffffffffu, s, of);
-        if (lane == 0) rho[c0 + cc] = s;
-      }
-      __syncthreads();
+      for (int of = 16; of > 0; of >>= 1) s += __shfl_xor_sync(0xffffffffu, s, of);
+      if (lane == 0) rho[c] = s;
     }
     if (mom_prev && wp < 3) {
       double s = 0.0;
