@@ -1,7 +1,10 @@
 // capi.cu -- error plumbing, basis upload and small utility entry points.
 #include <atomic>
 #include <cstdio>
+#include <map>
+#include <mutex>
 #include <string>
+#include <tuple>
 
 #include "sldg_common.cuh"
 
@@ -18,6 +21,46 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+std::mutex g_cfg_mu;
+std::map<std::tuple<const void*, int, int>, int> g_smem_set;          // (k, dev, bytes)
+std::map<std::tuple<const void*, int, int, int>, int> g_resident;     // (k, dev, thr, smem)
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+}  // namespace
+
+cudaError_t smem_limit(const void* kernel, int bytes) {
+  const auto key = std::make_tuple(kernel, current_device(), bytes);
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  if (g_smem_set.count(key)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) g_smem_set[key] = 1;
+  return e;
+}
+
+cudaError_t resident_ctas(const void* kernel, int threads, int smem, int* per_sm) {
+  const int dev = current_device();
+  const auto key = std::make_tuple(kernel, dev, threads, smem);
+  {
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
+    auto it = g_resident.find(key);
+    if (it != g_resident.end()) {
+      *per_sm = it->second;
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = smem_limit(kernel, smem);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kernel, threads, (size_t)smem);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  g_resident[key] = *per_sm;
+  return cudaSuccess;
+}
 
 bool make_dev_basis(const SldgBasis& b, DevBasis* out, std::string* err) {
   if (b.degree < 1 || b.degree > SLDG_MAX_DEGREE) {

@@ -729,9 +729,8 @@ static FusedKernel fused_kernel(const sldg_vplan* vp, const sldg_xplan* xp, cons
 
 // resident persistent grid (deterministic for a device): partial rows written
 static int fused_grid(FusedKernel k, const FusedGeom& g, long long* grid) {
-  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
   int per_sm = 0;
-  SLDG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, g.threads, g.smem));
+  SLDG_CUDA_TRY(resident_ctas((const void*)k, g.threads, (int)g.smem, &per_sm));
   *grid = std::max<long long>(1, std::min<long long>(g.grid, (long long)std::max(per_sm, 1) * sm_count()));
   return SLDG_OK;
 }
@@ -1018,9 +1017,8 @@ int sldg_step_fused_advice(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n
   // degree-3 velocity or x bases) the separate passes are as fast or faster
   cudaFuncAttributes attr;
   SLDG_CUDA_TRY(cudaFuncGetAttributes(&attr, k));
-  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
   int per_sm = 0;
-  SLDG_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, g.threads, g.smem));
+  SLDG_CUDA_TRY(resident_ctas((const void*)k, g.threads, (int)g.smem, &per_sm));
   *profitable = (attr.localSizeBytes == 0 && per_sm >= 2) ? 1 : 0;
   return SLDG_OK;
 }

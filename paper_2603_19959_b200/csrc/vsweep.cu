@@ -375,8 +375,7 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
     const int threads = (tx_max + 31) / 32 * 32;
     const int rstride = whole ? (int)ld : tx_max;
     const size_t smem = sizeof(double) * (size_t)kStreamRing * NLOC * rstride;
-    SLDG_CUDA_TRY(cudaFuncSetAttribute(k_sweep_stream<O, DIM>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    SLDG_CUDA_TRY(smem_limit((const void*)k_sweep_stream<O, DIM>, (int)smem));
     const int n_tiles = (int)((n_cols + tx_max - 1) / tx_max);
     const long long blocks = p->n_walk * n_tiles;
     k_sweep_stream<O, DIM><<<(unsigned)blocks, threads, smem, st>>>(

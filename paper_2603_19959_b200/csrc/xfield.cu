@@ -305,8 +305,7 @@ static int launch_advect_x(const sldg_xplan* X, const double* fin, long long ld_
     set_error("x row too long for shared-memory staging");
     return SLDG_ERR_UNSUPPORTED;
   }
-  SLDG_CUDA_TRY(cudaFuncSetAttribute(k_advect_x<O>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)std::max<size_t>(smem, 48 * 1024)));
+  SLDG_CUDA_TRY(smem_limit((const void*)k_advect_x<O>, (int)std::max<size_t>(smem, 48 * 1024)));
   long long blocks = (X->n_rows + rows - 1) / rows;
   k_advect_x<O><<<(unsigned)blocks, 256, smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
                                                      in_cells, out_cells, halo_l, periodic, rows);
@@ -394,16 +393,14 @@ static int launch_xadv_t(const sldg_xplan* X, const double* fin, long long ld_in
                          cudaStream_t st) {
   if (g.cpcm < 0) {
     auto kc = g.cpcm == -8 ? k_xadv_c<O, NAPPLY, MOM, RHO, 8> : k_xadv_c<O, NAPPLY, MOM, RHO, 16>;
-    SLDG_CUDA_TRY(cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)std::max<size_t>(g.smem, 48 * 1024)));
+    SLDG_CUDA_TRY(smem_limit((const void*)kc, (int)std::max<size_t>(g.smem, 48 * 1024)));
     kc<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
                                            (int)X->n_cells, (int)X->n_speeds, epi);
     SLDG_LAUNCH_CHECK("k_xadv_c");
     return SLDG_OK;
   }
   auto k = g.cpcm == 8 ? k_xadv<O, NAPPLY, MOM, RHO, 8> : k_xadv<O, NAPPLY, MOM, RHO, 16>;
-  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)std::max<size_t>(g.smem, 48 * 1024)));
+  SLDG_CUDA_TRY(smem_limit((const void*)k, (int)std::max<size_t>(g.smem, 48 * 1024)));
   k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
                                         (int)X->n_cells, (int)X->n_speeds, g.tab_smem ? 1 : 0,
                                         epi);
@@ -495,7 +492,7 @@ static int launch_xt_t(const sldg_xplan* X, const XTGeom& g, const double* fin, 
   if constexpr (OV == 3) {
     if (g.rpt == 3) k = k_xx_tiles<OV, OX, 3>;
   }
-  SLDG_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+  SLDG_CUDA_TRY(smem_limit((const void*)k, (int)g.smem));
   k<<<(unsigned)g.grid_, g.threads, g.smem, st>>>(X->dev, fin, fout, ld, X->n_rows, g.n_out,
                                                   g.rpt, g.tpc, g.nring, (int)X->n_speeds, epi,
                                                   napply, mom ? 1 : 0, rho ? 1 : 0, rm);
