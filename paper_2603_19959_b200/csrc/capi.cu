@@ -24,7 +24,7 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 namespace {
 std::mutex g_cfg_mu;
-std::map<std::tuple<const void*, int, int>, int> g_smem_set;          // (k, dev, bytes)
+std::map<std::pair<const void*, int>, int> g_smem_set;   // (k, dev) -> largest limit set
 std::map<std::tuple<const void*, int, int, int>, int> g_resident;     // (k, dev, thr, smem)
 int current_device() {
   int d = 0;
@@ -34,11 +34,14 @@ int current_device() {
 }  // namespace
 
 cudaError_t smem_limit(const void* kernel, int bytes) {
-  const auto key = std::make_tuple(kernel, current_device(), bytes);
+  // the attribute is a per-function maximum: only ever raise it, so a smaller
+  // request after a larger one cannot lower the limit under a cached larger key
+  const auto key = std::make_pair(kernel, current_device());
   std::lock_guard<std::mutex> lk(g_cfg_mu);
-  if (g_smem_set.count(key)) return cudaSuccess;
+  auto it = g_smem_set.find(key);
+  if (it != g_smem_set.end() && it->second >= bytes) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) g_smem_set[key] = 1;
+  if (e == cudaSuccess) g_smem_set[key] = bytes;
   return e;
 }
 
