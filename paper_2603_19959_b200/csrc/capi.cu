@@ -24,6 +24,7 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 namespace {
 std::mutex g_cfg_mu;
+std::map<int, int> g_sms;                                  // dev -> SM count
 std::map<std::pair<const void*, int>, int> g_smem_set;   // (k, dev) -> largest limit set
 std::map<std::tuple<const void*, int, int, int>, int> g_resident;     // (k, dev, thr, smem)
 int current_device() {
@@ -63,6 +64,18 @@ cudaError_t resident_ctas(const void* kernel, int threads, int smem, int* per_sm
   std::lock_guard<std::mutex> lk(g_cfg_mu);
   g_resident[key] = *per_sm;
   return cudaSuccess;
+}
+
+int num_sms() {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  auto it = g_sms.find(dev);
+  if (it != g_sms.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    n = 148;
+  g_sms[dev] = n;
+  return n;
 }
 
 bool make_dev_basis(const SldgBasis& b, DevBasis* out, std::string* err) {

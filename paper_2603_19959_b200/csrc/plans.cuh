@@ -25,7 +25,7 @@ struct VPlanDev {
   const double* c_weight;
   const long long* walk_pencils;  // whole-fast pencils, for k_sweep_walk
   const long long* walk_desc;     // per walk position: {p_off, p_n | level << 32}
-  const long long* gen_entries;   // entries handled by k_sweep_generic when walk is used
+  const long long* gen_entries;   // entries of the per-cell worklist when walk is used
   long long n_entries, n_targets, n_walk, n_gen;
   int stride_d, stride_t0, stride_t1;
   int n_levels;

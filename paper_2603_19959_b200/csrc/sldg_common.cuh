@@ -37,10 +37,11 @@ int cuda_fail(cudaError_t e, const char* what);
 void count_launch(int n = 1);
 // Launch configuration without per-launch driver queries (so a launch sequence can be
 // captured into a CUDA graph and replayed without host work): the dynamic shared
-// memory limit of a kernel is raised once per (kernel, device, bytes), and the
-// resident CTAs per SM are memoised (capi.cu).
+// memory limit of a kernel is only ever raised, the resident CTAs per SM and the SM
+// count are memoised (capi.cu).
 cudaError_t smem_limit(const void* kernel, int bytes);
 cudaError_t resident_ctas(const void* kernel, int threads, int smem, int* per_sm);
+int num_sms();
 
 #define SLDG_CUDA_TRY(expr)                               \
   do {                                                    \

@@ -18,9 +18,11 @@
 //   k_sweep_walk      whole-pencil-fast pencils: a CTA walks one pencil over
 //                     an x tile, streaming each cell once from HBM through a
 //                     shared-memory ring (cp.async), 16 B/DOF
-//   k_sweep_generic   every other entry: per-cell fast path with the O(1)
-//                     same-level-run check, or the slow path (generalized
-//                     overlap by on-the-fly Gauss quadrature)
+//   k_vclassify       every other (entry, column): per-cell fast check (O(1)
+//                     same-level runs) -> FAST / SLOW device worklists
+//   k_vitems          persistent warps drain the worklists (slow first): the
+//                     per-cell fast path, or the slow path (generalized overlap
+//                     by on-the-fly Gauss quadrature)
 //   k_writeback       weighted targets: f_in + sum_g sum_k w (r_k - f_in) in the
 //                     reference's summation order (no atomics)
 #include <algorithm>
@@ -41,8 +43,9 @@ template <int O>
 __global__ void k_level_mats(DevBasis b, const double* __restrict__ speeds, long long n_cols,
                              double dt, double base_width, int n_levels,
                              long long* __restrict__ lm_ns, double* __restrict__ lm_frac,
-                             double* __restrict__ lm_mats) {
+                             double* __restrict__ lm_mats, unsigned* __restrict__ wl_cnt) {
   long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (wl_cnt && idx < 4) wl_cnt[idx] = 0u;   // the per-cell worklist counters of this sweep
   if (idx >= n_cols * n_levels) return;
   int lev = (int)(idx / n_cols);
   long long c = idx - (long long)lev * n_cols;
@@ -93,74 +96,145 @@ __device__ __forceinline__ void general_block(const DevBasis& b, double vl, doub
   apply_minv<O>(b, raw, M);
 }
 
-// One (entry, column): writes the entry's NLOC outputs for column c.
+// ---------------------------------------------------------------------------
+// Per-cell entries (AMR boundary pencils, single-cell pencils, forced slow):
+// a device-side worklist.
+//
+// k_vclassify  thread = (entry, column).  Exact-zero speed columns are copied
+//              here (vsweep.py:429-431); otherwise the per-cell fast check
+//              (_fast_sources_ok, vsweep.py:205-219) files the item in the FAST
+//              or the SLOW list.  A warp reserves 32 consecutive slots in each
+//              list it contributes to (one atomic per warp and list; lanes with
+//              nothing to file write kNoItem), so a list chunk is one warp's
+//              consecutive columns of (mostly) one entry: coalesced downstream.
+// k_vitems     persistent warps pull units (chunk x line group) from a device
+//              counter, SLOW units first (the expensive ones), then FAST units,
+//              so the load is balanced whatever the slow/fast mix and the cost of
+//              each item is uniform across its warp.  A slow unit re-derives the
+//              foot segments and evaluates each generalized overlap block by
+//              on-the-fly Gauss quadrature (vsweep.py:221-245) once per line
+//              group; outputs accumulate in registers in the reference's order
+//              (sources ascending per foot segment, vsweep.py:244-245) and are
+//              stored once.
+// Both are deterministic: every output is produced by one thread, in a fixed
+// order; the list order only decides which warp does the work.
+// ---------------------------------------------------------------------------
+constexpr unsigned kNoItem = 0xffffffffu;
+
+// a per-cell item's destination: f_out rows, or its weighted-entry scratch slot
 template <int O, int DIM>
-__device__ __forceinline__ void sweep_entry(const VPlanDev& P, const DevBasis& b,
-                                            const double* __restrict__ fin,
-                                            double* __restrict__ fout, long long ld,
+__device__ __forceinline__ double* item_dst(const VPlanDev& P, double* fout, long long ld,
                                             long long n_cols, long long e, long long c,
-                                            double speed, double dt, int bc, int force_slow,
-                                            const long long* __restrict__ lm_ns,
-                                            const double* __restrict__ lm_mats,
-                                            double* __restrict__ acc) {
+                                            double* acc, long long* dstride) {
+  const int slot = P.e_slot[e];
+  if (slot < 0) {
+    *dstride = ld;
+    return fout + P.e_row0[e] * ld + c;
+  }
+  *dstride = n_cols;
+  return acc + (long long)slot * Lines<O, DIM>::NLOC * n_cols + c;
+}
+
+template <int O, int DIM>
+__global__ void __launch_bounds__(256)
+k_vclassify(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout, long long ld,
+            long long n_cols, const double* __restrict__ speeds, int bc, int force_slow,
+            const long long* __restrict__ lm_ns, double* __restrict__ acc, long long n_items,
+            int use_list, unsigned* __restrict__ cnt, unsigned* __restrict__ list_f,
+            unsigned* __restrict__ list_s) {
+  using L = Lines<O, DIM>;
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int kind = 0;   // 0: nothing to file (out of range / copied), 1: fast, 2: slow
+  if (idx < n_items * n_cols) {
+    const long long item = idx / n_cols;
+    const long long c = idx - item * n_cols;
+    const long long e = use_list ? P.gen_entries[item] : item;
+    if (__ldg(speeds + c) == 0.0) {   // exact-zero speed: untouched bits
+      long long dstride;
+      double* dst = item_dst<O, DIM>(P, fout, ld, n_cols, e, c, acc, &dstride);
+      const double* self = fin + P.e_row0[e] * ld + c;
+      for (int r = 0; r < L::NLOC; ++r) dst[r * dstride] = self[r * ld];
+    } else if (force_slow) {
+      kind = 2;
+    } else {
+      const int q = P.e_pencil[e];
+      if (P.p_fast[q]) {
+        kind = 1;
+      } else if (P.e_conf[e]) {
+        const long long ns = lm_ns[(long long)P.e_level[e] * n_cols + c];
+        kind = sources_ok(P.e_runs + 4 * e, (int)(e - P.p_off[q]), ns, P.p_n[q], bc) ? 1 : 2;
+      } else {
+        kind = 2;
+      }
+    }
+  }
+  const unsigned mf = __ballot_sync(~0u, kind == 1), ms = __ballot_sync(~0u, kind == 2);
+  unsigned bf = 0, bs = 0;
+  if (lane == 0) {
+    if (mf) bf = atomicAdd(cnt + 0, 32u);
+    if (ms) bs = atomicAdd(cnt + 1, 32u);
+  }
+  bf = __shfl_sync(~0u, bf, 0);
+  bs = __shfl_sync(~0u, bs, 0);
+  if (mf) list_f[bf + lane] = kind == 1 ? (unsigned)idx : kNoItem;
+  if (ms) list_s[bs + lane] = kind == 2 ? (unsigned)idx : kNoItem;
+}
+
+// per-cell fast path (vsweep.py:205-219) for the LPG lines of group g
+template <int O, int DIM, int LPG>
+__device__ __forceinline__ void fast_group(const VPlanDev& P, const double* __restrict__ fin,
+                                           long long ld, long long n_cols, long long e,
+                                           long long c, int g, int bc,
+                                           const long long* __restrict__ lm_ns,
+                                           const double* __restrict__ lm_mats, double* dst,
+                                           long long dstride) {
   using L = Lines<O, DIM>;
   const int q = P.e_pencil[e];
   const long long off = P.p_off[q];
   const int n = P.p_n[q];
   const int s = (int)(e - off);
-  const int slot = P.e_slot[e];
-  double* dst;
-  long long dstride;
-  if (slot < 0) {
-    dst = fout + P.e_row0[e] * ld + c;
-    dstride = ld;
-  } else {
-    dst = acc + (long long)slot * L::NLOC * n_cols + c;
-    dstride = n_cols;
-  }
-  const double* self = fin + P.e_row0[e] * ld + c;
-  if (speed == 0.0) {   // exact-zero speed: untouched bits (vsweep.py:429-431)
-    for (int r = 0; r < L::NLOC; ++r) dst[r * dstride] = self[r * ld];
-    return;
-  }
   const int lev = P.e_level[e];
   const long long ns = lm_ns[(long long)lev * n_cols + c];
-  bool fast = false;
-  if (!force_slow) {
-    if (P.p_fast[q]) fast = true;
-    else if (P.e_conf[e]) fast = sources_ok(P.e_runs + 4 * e, s, ns, n, bc);
+  double A[O * O], B[O * O];
+  load_pair<O>(lm_mats, lev, n_cols, c, A, B);
+  long long qa = s - ns, qb = s - ns - 1;
+  bool va = true, vb = true;
+  if (bc == SLDG_BC_PERIODIC) {
+    qa = pymod(qa, n);
+    qb = pymod(qb, n);
+  } else {
+    va = (qa >= 0 && qa < n);
+    vb = (qb >= 0 && qb < n);
   }
-  if (fast) {
-    double A[O * O], B[O * O];
-    load_pair<O>(lm_mats, lev, n_cols, c, A, B);
-    long long qa = s - ns, qb = s - ns - 1;
-    bool va = true, vb = true;
-    if (bc == SLDG_BC_PERIODIC) {
-      qa = pymod(qa, n);
-      qb = pymod(qb, n);
-    } else {
-      va = (qa >= 0 && qa < n);
-      vb = (qb >= 0 && qb < n);
-    }
-    const double* pa = fin + (va ? P.e_row0[off + qa] : 0) * ld + c;
-    const double* pb = fin + (vb ? P.e_row0[off + qb] : 0) * ld + c;
-#pragma unroll 1
-    for (int t = 0; t < L::NL; ++t) {
-      double ua[O], ub[O], y[O];
+  const double* pa = fin + (va ? P.e_row0[off + qa] : 0) * ld + c;
+  const double* pb = fin + (vb ? P.e_row0[off + qb] : 0) * ld + c;
 #pragma unroll
-      for (int i = 0; i < O; ++i) {
-        int r = L::row(P, t, i);
-        ua[i] = va ? pa[(long long)r * ld] : 0.0;
-        ub[i] = vb ? pb[(long long)r * ld] : 0.0;
-      }
-      two_cell<O>(A, B, ua, ub, va, vb, y);
+  for (int k = 0; k < LPG; ++k) {
+    const int t = g * LPG + k;
+    double ua[O], ub[O], y[O];
 #pragma unroll
-      for (int i = 0; i < O; ++i) dst[(long long)L::row(P, t, i) * dstride] = y[i];
+    for (int i = 0; i < O; ++i) {
+      const int r = L::row(P, t, i);
+      ua[i] = va ? pa[(long long)r * ld] : 0.0;
+      ub[i] = vb ? pb[(long long)r * ld] : 0.0;
     }
-    return;
+    two_cell<O>(A, B, ua, ub, va, vb, y);
+#pragma unroll
+    for (int i = 0; i < O; ++i) dst[(long long)L::row(P, t, i) * dstride] = y[i];
   }
+}
 
-  // ---- slow path (vsweep.py:221-245) ----
+// slow path (vsweep.py:221-245) for the LPG lines of group g
+template <int O, int DIM, int LPG>
+__device__ __forceinline__ void slow_group(const VPlanDev& P, const DevBasis& b,
+                                           const double* __restrict__ fin, long long ld,
+                                           long long e, long long c, int g, double speed,
+                                           double dt, int bc, double* dst, long long dstride) {
+  using L = Lines<O, DIM>;
+  const int q = P.e_pencil[e];
+  const long long off = P.p_off[q];
+  const int n = P.p_n[q];
   const double disp = __dmul_rn(speed, dt);
   const double dlo = P.e_lower[e], dw = P.e_width[e];
   const double flo = __dsub_rn(dlo, disp);
@@ -189,6 +263,7 @@ __device__ __forceinline__ void sweep_entry(const VPlanDev& P, const DevBasis& b
   }
   const double* lows = P.e_lower + off;
   const double* wids = P.e_width + off;
+  double y[LPG][O];
   bool first = true;
   for (int pc = 0; pc < npieces; ++pc) {
     const double a = pa_[pc], z = pz_[pc], de = pd_[pc];
@@ -211,42 +286,75 @@ __device__ __forceinline__ void sweep_entry(const VPlanDev& P, const DevBasis& b
       double M[O * O];
       general_block<O>(b, vl, vr, dlo, dw, slo, sw, de, M);
       const double* src = fin + P.e_row0[off + cc] * ld + c;
-#pragma unroll 1
-      for (int t = 0; t < L::NL; ++t) {
+#pragma unroll
+      for (int k = 0; k < LPG; ++k) {
+        const int t = g * LPG + k;
         double u[O];
 #pragma unroll
         for (int i = 0; i < O; ++i) u[i] = src[(long long)L::row(P, t, i) * ld];
 #pragma unroll
         for (int i = 0; i < O; ++i) {
-          double y = M[i * O] * u[0];
+          double r = M[i * O] * u[0];
 #pragma unroll
-          for (int j = 1; j < O; ++j) y = fma(M[i * O + j], u[j], y);
-          double* d = dst + (long long)L::row(P, t, i) * dstride;
-          *d = first ? y : (*d + y);
+          for (int j = 1; j < O; ++j) r = fma(M[i * O + j], u[j], r);
+          y[k][i] = first ? r : __dadd_rn(y[k][i], r);
         }
       }
       first = false;
     }
   }
-  if (first) {   // no source overlaps (absorbed): zero
-    for (int r = 0; r < L::NLOC; ++r) dst[r * dstride] = 0.0;
+#pragma unroll
+  for (int k = 0; k < LPG; ++k) {
+    const int t = g * LPG + k;
+#pragma unroll
+    for (int i = 0; i < O; ++i)   // no source overlaps (absorbed): zero
+      dst[(long long)L::row(P, t, i) * dstride] = first ? 0.0 : y[k][i];
   }
 }
 
 template <int O, int DIM>
+struct ItemGroups {
+  static constexpr int LPG = DIM == 3 ? O : 1;         // lines per unit
+  static constexpr int NG = Lines<O, DIM>::NL / LPG;   // units per list chunk
+};
+
+template <int O, int DIM>
 __global__ void __launch_bounds__(128)
-k_sweep_generic(VPlanDev P, DevBasis b, const double* __restrict__ fin,
-                double* __restrict__ fout, long long ld, long long n_cols,
-                const double* __restrict__ speeds, double dt, int bc, int force_slow,
-                const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
-                double* __restrict__ acc, long long n_items, int use_list) {
-  long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= n_items * n_cols) return;
-  long long item = idx / n_cols;
-  long long c = idx - item * n_cols;
-  long long e = use_list ? P.gen_entries[item] : item;
-  sweep_entry<O, DIM>(P, b, fin, fout, ld, n_cols, e, c, __ldg(speeds + c), dt, bc, force_slow,
-                      lm_ns, lm_mats, acc);
+k_vitems(VPlanDev P, DevBasis b, const double* __restrict__ fin, double* __restrict__ fout,
+         long long ld, long long n_cols, const double* __restrict__ speeds, double dt, int bc,
+         const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
+         double* __restrict__ acc, int use_list, unsigned* __restrict__ cnt,
+         const unsigned* __restrict__ list_f, const unsigned* __restrict__ list_s) {
+  using IG = ItemGroups<O, DIM>;
+  const int lane = threadIdx.x & 31;
+  const unsigned n_slow = __ldcg(cnt + 1) / 32u * IG::NG;
+  const unsigned n_units = n_slow + __ldcg(cnt + 0) / 32u * IG::NG;
+  const unsigned nc = (unsigned)n_cols;
+  for (;;) {
+    unsigned u = 0;
+    if (lane == 0) u = atomicAdd(cnt + 2, 1u);
+    u = __shfl_sync(~0u, u, 0);
+    if (u >= n_units) break;
+    const bool slow = u < n_slow;
+    const unsigned v = slow ? u : u - n_slow;
+    const unsigned chunk = v / IG::NG;
+    const int g = (int)(v - chunk * IG::NG);
+    const unsigned it = (slow ? list_s : list_f)[chunk * 32u + lane];
+    if (it != kNoItem) {
+      const unsigned item = it / nc;
+      const long long c = it - item * nc;
+      const long long e = use_list ? P.gen_entries[item] : (long long)item;
+      long long dstride;
+      double* dst = item_dst<O, DIM>(P, fout, ld, n_cols, e, c, acc, &dstride);
+      if (slow)
+        slow_group<O, DIM, IG::LPG>(P, b, fin, ld, e, c, g, __ldg(speeds + c), dt, bc, dst,
+                                    dstride);
+      else
+        fast_group<O, DIM, IG::LPG>(P, fin, ld, n_cols, e, c, g, bc, lm_ns, lm_mats, dst,
+                                    dstride);
+    }
+    __syncwarp();
+  }
 }
 
 }  // namespace sldg
@@ -257,18 +365,23 @@ namespace sldg {
 
 // weighted write-back (vsweep.py:403-409): out = ((f_in + S_g1) + S_g2) + ...,
 // S_g = sum over the group's contributions in flat order of w (r - f_in).
-// Block x = one target cell (its contribution list staged in shared memory once),
-// block y * blockDim + thread = column, each thread walks the cell's NLOC rows.
+// Block x = (target cell, group of RPT rows), its contribution list staged in shared
+// memory once; block y * blockDim + thread = column.  A thread carries RPT independent
+// row sums through the contribution loop (RPT loads in flight per contribution), each
+// in the reference's order.
 constexpr int kWbMaxC = 32;   // contributions per target staged in shared memory
+constexpr int kWbRows = 4;    // rows per thread
 
-template <int NLOC>
-__global__ void __launch_bounds__(256)
+template <int NLOC, int RPT>
+__global__ void __launch_bounds__(128)
 k_writeback(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout, long long ld,
             long long n_cols, const double* __restrict__ speeds, const double* __restrict__ acc) {
+  constexpr int NRG = (NLOC + RPT - 1) / RPT;
   __shared__ const double* s_src[kWbMaxC];   // acc row 0 of each contribution's slot
   __shared__ int s_grp[kWbMaxC];
   __shared__ double s_w[kWbMaxC];
-  const long long t = blockIdx.x;
+  const long long t = blockIdx.x / NRG;
+  const int r0 = (int)(blockIdx.x - t * NRG) * RPT;
   const long long k0 = P.t_off[t];
   const int nk = (int)(P.t_off[t + 1] - k0);
   const int ns = min(nk, kWbMaxC);
@@ -280,33 +393,44 @@ k_writeback(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fou
   __syncthreads();
   const long long c = (long long)blockIdx.y * blockDim.x + threadIdx.x;
   if (c >= n_cols) return;
-  const bool moving = __ldg(speeds + c) != 0.0;
-  const long long row0 = P.t_row0[t];
-#pragma unroll 3
-  for (int r = 0; r < NLOC; ++r) {
-    const long long at = (row0 + r) * ld + c;
-    const double fv = fin[at];
-    if (!moving) {   // exact-zero speed: untouched bits
-      fout[at] = fv;
-      continue;
-    }
-    double o = fv, s = 0.0;
+  const double* fin_c = fin + P.t_row0[t] * ld + c;
+  double* fout_c = fout + P.t_row0[t] * ld + c;
+  double fv[RPT], o[RPT], sm[RPT];
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr) {
+    const int r = r0 + rr;
+    fv[rr] = (r < NLOC) ? fin_c[(long long)r * ld] : 0.0;
+    o[rr] = fv[rr];
+    sm[rr] = 0.0;
+  }
+  if (__ldg(speeds + c) != 0.0) {   // exact-zero speed: untouched bits
     int g = s_grp[0];
     for (int k = 0; k < nk; ++k) {
       const bool sh = k < kWbMaxC;
       const int gk = sh ? s_grp[k] : P.c_group[k0 + k];
       if (gk != g) {
-        o = __dadd_rn(o, s);
-        s = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < RPT; ++rr) {
+          o[rr] = __dadd_rn(o[rr], sm[rr]);
+          sm[rr] = 0.0;
+        }
         g = gk;
       }
-      const double* src = sh ? s_src[k] : acc + (long long)P.c_slot[k0 + k] * NLOC * n_cols;
+      const double* src = (sh ? s_src[k] : acc + (long long)P.c_slot[k0 + k] * NLOC * n_cols) + c;
       const double wk = sh ? s_w[k] : P.c_weight[k0 + k];
-      const double rv = src[(long long)r * n_cols + c];
-      s = __dadd_rn(s, __dmul_rn(wk, __dsub_rn(rv, fv)));
+#pragma unroll
+      for (int rr = 0; rr < RPT; ++rr) {
+        const int r = r0 + rr;
+        const double rv = (r < NLOC) ? src[(long long)r * n_cols] : 0.0;
+        sm[rr] = __dadd_rn(sm[rr], __dmul_rn(wk, __dsub_rn(rv, fv[rr])));
+      }
     }
-    fout[at] = __dadd_rn(o, s);
+#pragma unroll
+    for (int rr = 0; rr < RPT; ++rr) o[rr] = __dadd_rn(o[rr], sm[rr]);
   }
+#pragma unroll
+  for (int rr = 0; rr < RPT; ++rr)
+    if (r0 + rr < NLOC) fout_c[(long long)(r0 + rr) * ld] = o[rr];
 }
 
 // ---------------------------------------------------------------------------
@@ -315,7 +439,8 @@ k_writeback(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fou
 static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct ScratchLayout {
-  size_t ns_off, frac_off, mats_off, acc_off, total;
+  size_t ns_off, frac_off, mats_off, acc_off, cnt_off, lf_off, ls_off, total;
+  long long list_cap;   // slots per worklist (warp-padded per-cell items)
 };
 
 static ScratchLayout scratch_layout(const sldg_vplan* p, long long n_cols) {
@@ -329,6 +454,15 @@ static ScratchLayout scratch_layout(const sldg_vplan* p, long long n_cols) {
   off = align_up(off + sizeof(double) * p->dev.n_levels * 2 * p->o * p->o * n_cols, 256);
   L.acc_off = off;
   off = align_up(off + sizeof(double) * (size_t)p->n_slots * p->n_local * n_cols, 256);
+  // per-cell worklists: every (entry, column) of the generic path at most once, in
+  // chunks of 32 (one per classifying warp and list)
+  L.list_cap = (p->n_entries * n_cols + 31) / 32 * 32;
+  L.cnt_off = off;
+  off = align_up(off + sizeof(unsigned) * 4, 256);
+  L.lf_off = off;
+  off = align_up(off + sizeof(unsigned) * (size_t)L.list_cap, 256);
+  L.ls_off = off;
+  off = align_up(off + sizeof(unsigned) * (size_t)L.list_cap, 256);
   L.total = off;
   return L;
 }
@@ -336,13 +470,13 @@ static ScratchLayout scratch_layout(const sldg_vplan* p, long long n_cols) {
 template <int O>
 static int launch_level_mats(const sldg_vplan* p, const double* speeds, long long n_cols,
                              double dt, long long* ns, double* frac, double* mats,
-                             cudaStream_t st) {
+                             unsigned* wl_cnt, cudaStream_t st) {
   long long n = n_cols * p->dev.n_levels;
   int threads = 128;
   long long blocks = (n + threads - 1) / threads;
   k_level_mats<O><<<(unsigned)blocks, threads, 0, st>>>(p->basis, speeds, n_cols, dt,
                                                        p->dev.base_width, p->dev.n_levels, ns,
-                                                       frac, mats);
+                                                       frac, mats, wl_cnt);
   SLDG_LAUNCH_CHECK("k_level_mats");
   return SLDG_OK;
 }
@@ -351,7 +485,7 @@ template <int O, int DIM>
 static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, long long ld,
                         long long n_cols, const double* speeds, double dt, int bc, int force_slow,
                         const long long* lm_ns, const double* lm_mats, double* acc,
-                        cudaStream_t st) {
+                        unsigned* wl_cnt, unsigned* list_f, unsigned* list_s, cudaStream_t st) {
   constexpr int NLOC = Lines<O, DIM>::NLOC;
   // streaming kernel geometry: whole rows per cell when the tile spans the row
   // (one bulk copy per cell), else column tiles with one bulk copy per row
@@ -381,24 +515,33 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
     k_sweep_stream<O, DIM><<<(unsigned)blocks, threads, smem, st>>>(
         p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, tx_max, n_tiles, whole);
     SLDG_LAUNCH_CHECK("k_sweep_stream");
-    if (p->n_gen > 0) {
-      long long n = p->n_gen * n_cols;
-      k_sweep_generic<O, DIM><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
-          p->dev, p->basis, fin, fout, ld, n_cols, speeds, dt, bc, force_slow, lm_ns, lm_mats,
-          acc, p->n_gen, 1);
-      SLDG_LAUNCH_CHECK("k_sweep_generic");
-    }
-  } else {
-    long long n = p->n_entries * n_cols;
-    k_sweep_generic<O, DIM><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
-        p->dev, p->basis, fin, fout, ld, n_cols, speeds, dt, bc, force_slow, lm_ns, lm_mats, acc,
-        p->n_entries, 0);
-    SLDG_LAUNCH_CHECK("k_sweep_generic");
+  }
+  // per-cell entries through the device worklist (classify, then balanced items)
+  const long long n_items = use_stream ? p->n_gen : p->n_entries;
+  if (n_items > 0) {
+    const long long n = n_items * n_cols;
+    k_vclassify<O, DIM><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        p->dev, fin, fout, ld, n_cols, speeds, bc, force_slow, lm_ns, acc, n_items,
+        use_stream ? 1 : 0, wl_cnt, list_f, list_s);
+    SLDG_LAUNCH_CHECK("k_vclassify");
+    int per_sm = 0;
+    SLDG_CUDA_TRY(resident_ctas((const void*)k_vitems<O, DIM>, 128, 0, &per_sm));
+    const long long max_units = (n + 31) / 32 * ItemGroups<O, DIM>::NG;   // one list full
+    const long long blocks =
+        std::max<long long>(1, std::min<long long>((long long)std::max(per_sm, 1) * num_sms(),
+                                                   (max_units + 3) / 4));
+    k_vitems<O, DIM><<<(unsigned)blocks, 128, 0, st>>>(p->dev, p->basis, fin, fout, ld, n_cols,
+                                                      speeds, dt, bc, lm_ns, lm_mats, acc,
+                                                      use_stream ? 1 : 0, wl_cnt, list_f,
+                                                      list_s);
+    SLDG_LAUNCH_CHECK("k_vitems");
   }
   if (p->n_targets > 0) {
-    const int threads = (int)std::min<long long>(256, (n_cols + 31) / 32 * 32);
-    const dim3 grid((unsigned)p->n_targets, (unsigned)((n_cols + threads - 1) / threads));
-    k_writeback<NLOC><<<grid, threads, 0, st>>>(p->dev, fin, fout, ld, n_cols, speeds, acc);
+    constexpr int NRG = (NLOC + kWbRows - 1) / kWbRows;
+    const int threads = (int)std::min<long long>(128, (n_cols + 31) / 32 * 32);
+    const dim3 grid((unsigned)(p->n_targets * NRG), (unsigned)((n_cols + threads - 1) / threads));
+    k_writeback<NLOC, kWbRows><<<grid, threads, 0, st>>>(p->dev, fin, fout, ld, n_cols, speeds,
+                                                          acc);
     SLDG_LAUNCH_CHECK("k_writeback");
   }
   return SLDG_OK;
@@ -714,7 +857,9 @@ int sldg_level_matrices(const sldg_vplan* p, const double* speeds, int64_t n_col
   cudaStream_t st = (cudaStream_t)stream;
   switch (p->o) {
 #define CASE(O) \
-  case O: return launch_level_mats<O>(p, speeds, n_cols, dt, (long long*)n_shift, frac, mats, st);
+  case O:                                                                               \
+    return launch_level_mats<O>(p, speeds, n_cols, dt, (long long*)n_shift, frac, mats,     \
+                                nullptr, st);
     CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
 #undef CASE
   }
@@ -752,18 +897,25 @@ int sldg_advect_v(const sldg_vplan* p, const double* fin, double* fout, int64_t 
   double* lm_frac = (double*)(sb + L.frac_off);
   double* lm_mats = (double*)(sb + L.mats_off);
   double* acc = (double*)(sb + L.acc_off);
+  unsigned* wl_cnt = (unsigned*)(sb + L.cnt_off);
+  unsigned* list_f = (unsigned*)(sb + L.lf_off);
+  unsigned* list_s = (unsigned*)(sb + L.ls_off);
+  if (L.list_cap >= (long long)kNoItem) {
+    set_error("advect_v: entries x columns exceed the 32-bit worklist index");
+    return SLDG_ERR_UNSUPPORTED;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   int rc = SLDG_ERR_UNSUPPORTED;
   switch (p->o) {
 #define CASE(O)                                                                               \
   case O:                                                                                     \
-    rc = launch_level_mats<O>(p, speeds, n_cols, dt, lm_ns, lm_frac, lm_mats, st);            \
+    rc = launch_level_mats<O>(p, speeds, n_cols, dt, lm_ns, lm_frac, lm_mats, wl_cnt, st);    \
     if (rc) return rc;                                                                        \
     if (p->dim == 3)                                                                          \
       return launch_sweep<O, 3>(p, fin, fout, ld, n_cols, speeds, dt, bc, force_slow, lm_ns,  \
-                                lm_mats, acc, st);                                            \
+                                lm_mats, acc, wl_cnt, list_f, list_s, st);                    \
     return launch_sweep<O, 1>(p, fin, fout, ld, n_cols, speeds, dt, bc, force_slow, lm_ns,    \
-                              lm_mats, acc, st);
+                              lm_mats, acc, wl_cnt, list_f, list_s, st);
     CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
 #undef CASE
   }
