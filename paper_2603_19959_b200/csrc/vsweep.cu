@@ -225,13 +225,14 @@ __device__ __forceinline__ void fast_group(const VPlanDev& P, const double* __re
   }
 }
 
-// slow path (vsweep.py:221-245) for the LPG lines of group g
-template <int O, int DIM, int LPG>
-__device__ __forceinline__ void slow_group(const VPlanDev& P, const DevBasis& b,
-                                           const double* __restrict__ fin, long long ld,
-                                           long long e, long long c, int g, double speed,
-                                           double dt, int bc, double* dst, long long dstride) {
-  using L = Lines<O, DIM>;
+// slow path (vsweep.py:221-245) of one (entry, column): foot segments, source cells by
+// binary search, sliver drop; apply(M, src, first) for every kept (segment, source) in the
+// reference's order.  Returns true when no source overlaps (absorbed: the output is 0).
+template <int O, class Apply>
+__device__ __forceinline__ bool slow_sources(const VPlanDev& P, const DevBasis& b,
+                                             const double* __restrict__ fin, long long ld,
+                                             long long e, long long c, double speed, double dt,
+                                             int bc, Apply&& apply) {
   const int q = P.e_pencil[e];
   const long long off = P.p_off[q];
   const int n = P.p_n[q];
@@ -263,7 +264,6 @@ __device__ __forceinline__ void slow_group(const VPlanDev& P, const DevBasis& b,
   }
   const double* lows = P.e_lower + off;
   const double* wids = P.e_width + off;
-  double y[LPG][O];
   bool first = true;
   for (int pc = 0; pc < npieces; ++pc) {
     const double a = pa_[pc], z = pz_[pc], de = pd_[pc];
@@ -285,37 +285,95 @@ __device__ __forceinline__ void slow_group(const VPlanDev& P, const DevBasis& b,
       if (!(__dsub_rn(vr, vl) > 1e-14 * dw)) continue;    // sliver drop (vsweep.py:230)
       double M[O * O];
       general_block<O>(b, vl, vr, dlo, dw, slo, sw, de, M);
-      const double* src = fin + P.e_row0[off + cc] * ld + c;
-#pragma unroll
-      for (int k = 0; k < LPG; ++k) {
-        const int t = g * LPG + k;
-        double u[O];
-#pragma unroll
-        for (int i = 0; i < O; ++i) u[i] = src[(long long)L::row(P, t, i) * ld];
-#pragma unroll
-        for (int i = 0; i < O; ++i) {
-          double r = M[i * O] * u[0];
-#pragma unroll
-          for (int j = 1; j < O; ++j) r = fma(M[i * O + j], u[j], r);
-          y[k][i] = first ? r : __dadd_rn(y[k][i], r);
-        }
-      }
+      apply(M, fin + P.e_row0[off + cc] * ld + c, first);
       first = false;
     }
   }
+  return first;
+}
+
+// r = M u for one line (the reference's src @ M.T row order)
+template <int O>
+__device__ __forceinline__ void mat_line(const double* M, const double* u, double* r) {
+#pragma unroll
+  for (int i = 0; i < O; ++i) {
+    double y = M[i * O] * u[0];
+#pragma unroll
+    for (int j = 1; j < O; ++j) y = fma(M[i * O + j], u[j], y);
+    r[i] = y;
+  }
+}
+
+// slow path for the LPG lines of group g, accumulators in registers
+template <int O, int DIM, int LPG>
+__device__ __forceinline__ void slow_group(const VPlanDev& P, const DevBasis& b,
+                                           const double* __restrict__ fin, long long ld,
+                                           long long e, long long c, int g, double speed,
+                                           double dt, int bc, double* dst, long long dstride) {
+  using L = Lines<O, DIM>;
+  double y[LPG][O];
+  const bool none = slow_sources<O>(P, b, fin, ld, e, c, speed, dt, bc,
+                                    [&](const double* M, const double* src, bool first) {
+#pragma unroll
+    for (int k = 0; k < LPG; ++k) {
+      const int t = g * LPG + k;
+      double u[O], r[O];
+#pragma unroll
+      for (int i = 0; i < O; ++i) u[i] = src[(long long)L::row(P, t, i) * ld];
+      mat_line<O>(M, u, r);
+#pragma unroll
+      for (int i = 0; i < O; ++i) y[k][i] = first ? r[i] : __dadd_rn(y[k][i], r[i]);
+    }
+  });
 #pragma unroll
   for (int k = 0; k < LPG; ++k) {
     const int t = g * LPG + k;
 #pragma unroll
-    for (int i = 0; i < O; ++i)   // no source overlaps (absorbed): zero
-      dst[(long long)L::row(P, t, i) * dstride] = first ? 0.0 : y[k][i];
+    for (int i = 0; i < O; ++i)
+      dst[(long long)L::row(P, t, i) * dstride] = none ? 0.0 : y[k][i];
   }
+}
+
+// slow path for all lines of the cell: each overlap block is formed once and applied
+// to every line; accumulators in shared memory (sacc[k * sstride], k = local row)
+template <int O, int DIM>
+__device__ __forceinline__ void slow_whole(const VPlanDev& P, const DevBasis& b,
+                                           const double* __restrict__ fin, long long ld,
+                                           long long e, long long c, double speed, double dt,
+                                           int bc, double* dst, long long dstride, double* sacc,
+                                           int sstride) {
+  using L = Lines<O, DIM>;
+  const bool none = slow_sources<O>(P, b, fin, ld, e, c, speed, dt, bc,
+                                    [&](const double* M, const double* src, bool first) {
+#pragma unroll 4
+    for (int t = 0; t < L::NL; ++t) {
+      double u[O], r[O];
+#pragma unroll
+      for (int i = 0; i < O; ++i) u[i] = src[(long long)L::row(P, t, i) * ld];
+      mat_line<O>(M, u, r);
+#pragma unroll
+      for (int i = 0; i < O; ++i) {
+        double* a = sacc + (t * O + i) * sstride;
+        *a = first ? r[i] : __dadd_rn(*a, r[i]);
+      }
+    }
+  });
+#pragma unroll 4
+  for (int t = 0; t < L::NL; ++t)
+#pragma unroll
+    for (int i = 0; i < O; ++i)
+      dst[(long long)L::row(P, t, i) * dstride] = none ? 0.0 : sacc[(t * O + i) * sstride];
 }
 
 template <int O, int DIM>
 struct ItemGroups {
-  static constexpr int LPG = DIM == 3 ? O : 1;         // lines per unit
-  static constexpr int NG = Lines<O, DIM>::NL / LPG;   // units per list chunk
+  static constexpr int LPG = DIM == 3 ? O : 1;         // lines per fast unit
+  static constexpr int NG = Lines<O, DIM>::NL / LPG;   // fast units per list chunk
+  // slow units: the whole cell (blocks formed once, shared-memory accumulators) while
+  // they fit three 128-thread CTAs per SM, else line groups like the fast units
+  static constexpr bool WHOLE = DIM == 3 && O <= 4;
+  static constexpr int NGS = WHOLE ? 1 : NG;
+  static constexpr int SMEM = WHOLE ? Lines<O, DIM>::NLOC * 128 * 8 : 0;
 };
 
 template <int O, int DIM>
@@ -326,8 +384,9 @@ k_vitems(VPlanDev P, DevBasis b, const double* __restrict__ fin, double* __restr
          double* __restrict__ acc, int use_list, unsigned* __restrict__ cnt,
          const unsigned* __restrict__ list_f, const unsigned* __restrict__ list_s) {
   using IG = ItemGroups<O, DIM>;
+  extern __shared__ __align__(16) double s_acc[];
   const int lane = threadIdx.x & 31;
-  const unsigned n_slow = __ldcg(cnt + 1) / 32u * IG::NG;
+  const unsigned n_slow = __ldcg(cnt + 1) / 32u * IG::NGS;
   const unsigned n_units = n_slow + __ldcg(cnt + 0) / 32u * IG::NG;
   const unsigned nc = (unsigned)n_cols;
   for (;;) {
@@ -337,8 +396,9 @@ k_vitems(VPlanDev P, DevBasis b, const double* __restrict__ fin, double* __restr
     if (u >= n_units) break;
     const bool slow = u < n_slow;
     const unsigned v = slow ? u : u - n_slow;
-    const unsigned chunk = v / IG::NG;
-    const int g = (int)(v - chunk * IG::NG);
+    const unsigned ng = slow ? IG::NGS : IG::NG;
+    const unsigned chunk = v / ng;
+    const int g = (int)(v - chunk * ng);
     const unsigned it = (slow ? list_s : list_f)[chunk * 32u + lane];
     if (it != kNoItem) {
       const unsigned item = it / nc;
@@ -346,11 +406,14 @@ k_vitems(VPlanDev P, DevBasis b, const double* __restrict__ fin, double* __restr
       const long long e = use_list ? P.gen_entries[item] : (long long)item;
       long long dstride;
       double* dst = item_dst<O, DIM>(P, fout, ld, n_cols, e, c, acc, &dstride);
-      if (slow)
-        slow_group<O, DIM, IG::LPG>(P, b, fin, ld, e, c, g, __ldg(speeds + c), dt, bc, dst,
-                                    dstride);
-      else
+      if (!slow)
         fast_group<O, DIM, IG::LPG>(P, fin, ld, n_cols, e, c, g, bc, lm_ns, lm_mats, dst,
+                                    dstride);
+      else if (IG::WHOLE)
+        slow_whole<O, DIM>(P, b, fin, ld, e, c, __ldg(speeds + c), dt, bc, dst, dstride,
+                           s_acc + threadIdx.x, 128);
+      else
+        slow_group<O, DIM, IG::LPG>(P, b, fin, ld, e, c, g, __ldg(speeds + c), dt, bc, dst,
                                     dstride);
     }
     __syncwarp();
@@ -524,13 +587,14 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
         p->dev, fin, fout, ld, n_cols, speeds, bc, force_slow, lm_ns, acc, n_items,
         use_stream ? 1 : 0, wl_cnt, list_f, list_s);
     SLDG_LAUNCH_CHECK("k_vclassify");
+    using IG = ItemGroups<O, DIM>;
     int per_sm = 0;
-    SLDG_CUDA_TRY(resident_ctas((const void*)k_vitems<O, DIM>, 128, 0, &per_sm));
-    const long long max_units = (n + 31) / 32 * ItemGroups<O, DIM>::NG;   // one list full
+    SLDG_CUDA_TRY(resident_ctas((const void*)k_vitems<O, DIM>, 128, IG::SMEM, &per_sm));
+    const long long max_units = (n + 31) / 32 * IG::NG;   // one list full
     const long long blocks =
         std::max<long long>(1, std::min<long long>((long long)std::max(per_sm, 1) * num_sms(),
                                                    (max_units + 3) / 4));
-    k_vitems<O, DIM><<<(unsigned)blocks, 128, 0, st>>>(p->dev, p->basis, fin, fout, ld, n_cols,
+    k_vitems<O, DIM><<<(unsigned)blocks, 128, IG::SMEM, st>>>(p->dev, p->basis, fin, fout, ld, n_cols,
                                                       speeds, dt, bc, lm_ns, lm_mats, acc,
                                                       use_stream ? 1 : 0, wl_cnt, list_f,
                                                       list_s);
