@@ -567,13 +567,17 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
       }
     if (tx_max > n_cols) tx_max = (int)((n_cols + 31) / 32 * 32);
   }
-  const bool use_stream = !force_slow && p->n_walk > 0 && tx_max > 0 && n_cols >= 2;
+  const int n_tiles = tx_max > 0 ? (int)((n_cols + tx_max - 1) / tx_max) : 0;
+  // the pencil walk runs one CTA per (pencil, column tile), each walking its pencil
+  // serially: below one CTA per SM it leaves the GPU idle, and the per-cell worklist
+  // (every cell of a whole-fast pencil is a fast item) is the faster schedule
+  const bool use_stream = !force_slow && p->n_walk > 0 && tx_max > 0 && n_cols >= 2 &&
+                          p->n_walk * n_tiles >= num_sms();
   if (use_stream) {
     const int threads = (tx_max + 31) / 32 * 32;
     const int rstride = whole ? (int)ld : tx_max;
     const size_t smem = sizeof(double) * (size_t)kStreamRing * NLOC * rstride;
     SLDG_CUDA_TRY(smem_limit((const void*)k_sweep_stream<O, DIM>, (int)smem));
-    const int n_tiles = (int)((n_cols + tx_max - 1) / tx_max);
     const long long blocks = p->n_walk * n_tiles;
     k_sweep_stream<O, DIM><<<(unsigned)blocks, threads, smem, st>>>(
         p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, tx_max, n_tiles, whole);
