@@ -209,19 +209,21 @@ __device__ __forceinline__ void fast_group(const VPlanDev& P, const double* __re
   }
   const double* pa = fin + (va ? P.e_row0[off + qa] : 0) * ld + c;
   const double* pb = fin + (vb ? P.e_row0[off + qb] : 0) * ld + c;
+  double ua[LPG][O], ub[LPG][O];   // all loads of the group before any store
 #pragma unroll
-  for (int k = 0; k < LPG; ++k) {
-    const int t = g * LPG + k;
-    double ua[O], ub[O], y[O];
+  for (int k = 0; k < LPG; ++k)
 #pragma unroll
     for (int i = 0; i < O; ++i) {
-      const int r = L::row(P, t, i);
-      ua[i] = va ? pa[(long long)r * ld] : 0.0;
-      ub[i] = vb ? pb[(long long)r * ld] : 0.0;
+      const int r = L::row(P, g * LPG + k, i);
+      ua[k][i] = va ? __ldg(pa + (long long)r * ld) : 0.0;
+      ub[k][i] = vb ? __ldg(pb + (long long)r * ld) : 0.0;
     }
-    two_cell<O>(A, B, ua, ub, va, vb, y);
 #pragma unroll
-    for (int i = 0; i < O; ++i) dst[(long long)L::row(P, t, i) * dstride] = y[i];
+  for (int k = 0; k < LPG; ++k) {
+    double y[O];
+    two_cell<O>(A, B, ua[k], ub[k], va, vb, y);
+#pragma unroll
+    for (int i = 0; i < O; ++i) dst[(long long)L::row(P, g * LPG + k, i) * dstride] = y[i];
   }
 }
 
@@ -345,16 +347,24 @@ __device__ __forceinline__ void slow_whole(const VPlanDev& P, const DevBasis& b,
   using L = Lines<O, DIM>;
   const bool none = slow_sources<O>(P, b, fin, ld, e, c, speed, dt, bc,
                                     [&](const double* M, const double* src, bool first) {
-#pragma unroll 4
-    for (int t = 0; t < L::NL; ++t) {
-      double u[O], r[O];
+    // lines in batches of O: the batch's loads are issued before any accumulator
+    // update (shared-memory stores would otherwise order the next global loads)
+#pragma unroll 1
+    for (int t0 = 0; t0 < L::NL; t0 += O) {
+      double u[O][O];
 #pragma unroll
-      for (int i = 0; i < O; ++i) u[i] = src[(long long)L::row(P, t, i) * ld];
-      mat_line<O>(M, u, r);
+      for (int k = 0; k < O; ++k)
 #pragma unroll
-      for (int i = 0; i < O; ++i) {
-        double* a = sacc + (t * O + i) * sstride;
-        *a = first ? r[i] : __dadd_rn(*a, r[i]);
+        for (int i = 0; i < O; ++i) u[k][i] = __ldg(src + (long long)L::row(P, t0 + k, i) * ld);
+#pragma unroll
+      for (int k = 0; k < O; ++k) {
+        double r[O];
+        mat_line<O>(M, u[k], r);
+#pragma unroll
+        for (int i = 0; i < O; ++i) {
+          double* a = sacc + ((t0 + k) * O + i) * sstride;
+          *a = first ? r[i] : __dadd_rn(*a, r[i]);
+        }
       }
     }
   });
@@ -377,7 +387,7 @@ struct ItemGroups {
 };
 
 template <int O, int DIM>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 3)   // three CTAs per SM (the shared-memory limit)
 k_vitems(VPlanDev P, DevBasis b, const double* __restrict__ fin, double* __restrict__ fout,
          long long ld, long long n_cols, const double* __restrict__ speeds, double dt, int bc,
          const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
