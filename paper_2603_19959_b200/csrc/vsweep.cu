@@ -26,6 +26,7 @@
 //   k_writeback       weighted targets: f_in + sum_g sum_k w (r_k - f_in) in the
 //                     reference's summation order (no atomics)
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -581,8 +582,13 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
   // the pencil walk runs one CTA per (pencil, column tile), each walking its pencil
   // serially: below one CTA per SM it leaves the GPU idle, and the per-cell worklist
   // (every cell of a whole-fast pencil is a fast item) is the faster schedule
-  const bool use_stream = !force_slow && p->n_walk > 0 && tx_max > 0 && n_cols >= 2 &&
-                          p->n_walk * n_tiles >= num_sms();
+  // SLDG_SWEEP_SCHEDULE=walk|items overrides the choice (tests: both schedules give
+  // the same bits)
+  const char* sched = std::getenv("SLDG_SWEEP_SCHEDULE");
+  const bool fills = sched && !std::strcmp(sched, "walk")    ? true
+                     : sched && !std::strcmp(sched, "items") ? false
+                                                             : p->n_walk * n_tiles >= num_sms();
+  const bool use_stream = !force_slow && p->n_walk > 0 && tx_max > 0 && n_cols >= 2 && fills;
   if (use_stream) {
     const int threads = (tx_max + 31) / 32 * 32;
     const int rstride = whole ? (int)ld : tx_max;
