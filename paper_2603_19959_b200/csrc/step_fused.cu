@@ -110,7 +110,11 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   const int n_cols = NXC > 0 ? OX * NXC : n_cols_arg;
   const int rw = NXC > 0 ? ((OX * NXC) | 1) : rw_arg;
   constexpr int XM = 2 * OX * OX;
-  constexpr int XCS = 3 * OX * OX + 2 * OX;     // composed x-step entries per v_x node
+  // composed x-step per v_x node: C0, C1, C2 (OX*OX each) then cA, cB (OX each),
+  // every block padded to an even count so the X phase reads them as 16-byte pairs
+  constexpr int XMP = (OX * OX + 1) & ~1, XZP = (OX + 1) & ~1;
+  constexpr int XCS = 3 * XMP + 2 * XZP;        // doubles per v_x node (even)
+  constexpr int XCL = 3 * OX * OX + 2 * OX;     // logical entries per v_x node
   constexpr int R = LG * OV;                    // rows per tile
   constexpr int n_lg = OV * OV / LG;
   extern __shared__ __align__(128) double sm[];
@@ -125,7 +129,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   int* xns = reinterpret_cast<int*>(xtab + (long long)n_speeds * XM);
   // composed x-step per tile and v_x node (MODE 0), two buffers alternating like
   // the tile buffers: C0 = A A, C1 = A B + B A, C2 = B B, then cA = A^T xw, cB = B^T xw
-  double* xcmp = xtab + (long long)n_speeds * XM + (n_speeds + 1) / 2;
+  double* xcmp = xtab + (long long)n_speeds * XM + 2 * ((n_speeds + 3) / 4);   // 16-byte aligned
   double* xw0 = xcmp + 2 * OV * XCS;            // x quadrature weights of one cell
   double* tabs0 = xw0 + OX;
   const int tab_dbl = nmax + 3 * R * nmax + (nmax * OV + 1) / 2;
@@ -448,12 +452,20 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
         double acc[LG][OX], zs[LG];
 #pragma unroll
         for (int m = 0; m < 3; ++m) {
-          double cm[OX * OX], cz[OX];
+          double cm[XMP], cz[XZP];
 #pragma unroll
-          for (int k = 0; k < OX * OX; ++k) cm[k] = Cc[m * OX * OX + k];
+          for (int k = 0; k < XMP; k += 2) {
+            const double2 q = *reinterpret_cast<const double2*>(Cc + m * XMP + k);
+            cm[k] = q.x;
+            cm[k + 1] = q.y;
+          }
           if (m < 2) {
 #pragma unroll
-            for (int k = 0; k < OX; ++k) cz[k] = Cc[3 * OX * OX + m * OX + k];
+            for (int k = 0; k < XZP; k += 2) {
+              const double2 q = *reinterpret_cast<const double2*>(Cc + 3 * XMP + m * XZP + k);
+              cz[k] = q.x;
+              cz[k + 1] = q.y;
+            }
           }
           const int pc = (m == 0 ? p0 : (m == 1 ? p1 : p2)) * OX;
 #pragma unroll
@@ -462,18 +474,20 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
             double uu[OX];
 #pragma unroll
             for (int j = 0; j < OX; ++j) uu[j] = u[j];
+            // one FMA chain per output across the three matrices (no separate
+            // partial sums: fewer instructions, same result to rounding)
 #pragma unroll
             for (int k = 0; k < OX; ++k) {
-              double sm_ = cm[k * OX] * uu[0];
+              double a = m == 0 ? cm[k * OX] * uu[0] : fma(cm[k * OX], uu[0], acc[t][k]);
 #pragma unroll
-              for (int j = 1; j < OX; ++j) sm_ = fma(cm[k * OX + j], uu[j], sm_);
-              acc[t][k] = m == 0 ? sm_ : acc[t][k] + sm_;
+              for (int j = 1; j < OX; ++j) a = fma(cm[k * OX + j], uu[j], a);
+              acc[t][k] = a;
             }
             if (m < 2) {
-              double zz = cz[0] * uu[0];
+              double zz = m == 0 ? cz[0] * uu[0] : fma(cz[0], uu[0], zs[t]);
 #pragma unroll
               for (int j = 1; j < OX; ++j) zz = fma(cz[j], uu[j], zz);
-              zs[t] = m == 0 ? zz : zs[t] + zz;
+              zs[t] = zz;
             }
           }
         }
@@ -527,13 +541,15 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     // MODE 0: composed x-step of cell s's v_x nodes -> dst (XCS entries per node)
     auto x_compose = [&](int s, double* dst) {
       if (MODE != 0) return;
-      for (int e0 = tid; e0 < OV * XCS; e0 += nthr) {   // the CTA may have < OV*XCS threads
-        const int jv = e0 / XCS, e = e0 - jv * XCS;
+      for (int e0 = tid; e0 < OV * XCL; e0 += nthr) {   // the CTA may have < OV*XCL threads
+        const int jv = e0 / XCL, e = e0 - jv * XCL;
+        int pos;   // padded position of logical entry e
         const double* A = xtab + (long long)T.cg[s * OV + jv] * XM;
         const double* B = A + OX * OX;
         double v;
         if (e < 3 * OX * OX) {
           const int w = e / (OX * OX), k = (e / OX) % OX, j = e % OX;
+          pos = w * XMP + k * OX + j;
           const double* L = w == 2 ? B : A;
           const double* Rm = w == 0 ? A : B;
           v = L[k * OX] * Rm[j];
@@ -545,12 +561,13 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
           }
         } else {
           const int q = e - 3 * OX * OX, j = q % OX;
+          pos = 3 * XMP + (q < OX ? 0 : XZP) + j;
           const double* M = q < OX ? A : B;
           v = xw0[0] * M[j];
 #pragma unroll
           for (int k = 1; k < OX; ++k) v = fma(xw0[k], M[k * OX + j], v);
         }
-        dst[e0] = v;
+        dst[jv * XCS + pos] = v;
       }
     };
     // one CTA barrier per tile; the next item's table prefetch advances one stage
@@ -659,7 +676,8 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   g.rw = (int)n_cols + (n_cols % 2 == 0 ? 1 : 0);   // odd row stride: conflict-free columns
   g.nmax = vp->max_walk_cells;
   const size_t fixed = sizeof(double) * (size_t)xp->n_speeds * 2 * OX * OX +
-                       sizeof(double) * ((xp->n_speeds + 1) / 2 + 2 * OV * (3 * OX * OX + 2 * OX) + OX) + 64;
+                       sizeof(double) * (2 * ((xp->n_speeds + 3) / 4) +
+                                         2 * OV * (3 * ((OX * OX + 1) & ~1) + 2 * ((OX + 1) & ~1)) + OX) + 64;
   const size_t nmax = (size_t)g.nmax;
   const size_t budget = 227 * 1024 - 1024;
   g.lg = 0;
