@@ -274,7 +274,10 @@ def run_ours(args):
                    "phase_dofs": dofs_total, "velocity_dofs": n_v,
                    "x_dofs": dofs_total // n_v, "bc": cfg.bc, "dt": cfg.dt,
                    "parallelism": parallelism,
-                   "l2": "inputs larger than L2 (state %.2f GB)" % (dofs_local * 8 / 1e9),
+                   "l2": ("inputs larger than L2 (state %.2f GB)" % (dofs_local * 8 / 1e9)
+                          if dofs_local * 8 > 126e6 else
+                          "state %.1f MB fits in the 126 MB L2, not flushed: a latency/throughput "
+                          "figure, not an HBM-roofline one (SURVEY 8d)" % (dofs_local * 8 / 1e6)),
                    "initial_data": "Landau f=(2pi)^-1.5 exp(-|v|^2/2)(1+0.01cos(0.5x))"},
         "pipeline": ("one HBM pass per step: k_step_fused (v-sweep + trailing half-x + "
                      "moments + next leading half-x + rho), 16 B/DOF" if fused else
