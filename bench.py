@@ -9,9 +9,9 @@ the launching stream, max over ranks.  f is 1.36 GB (> 126 MB L2), so every
 step streams from HBM; no L2 flush needed.
 
 Reference arm (--impl reference): the reference algorithm on the host's CPU
-cores (oracle/ port, all threads), on a bounded sample of the same workload
-(see cpu_sample()).  The reference is pure Python (nothing to compile), so the
-oracle restatement is what runs.
+cores (oracle/ port, all threads): whole Strang steps of the full state of the
+same config, wall-clock timed (CpuSteps).  The reference is pure Python (nothing
+to compile), so the oracle restatement is what runs.
 """
 from __future__ import annotations
 
@@ -135,6 +135,31 @@ class ClockSampler:
                 "samples": len(win), "window": note}
 
 
+def parallelism_for(config, world):
+    """(scaling, parallelism) of our arm at `world` ranks; the reference arm reports the same
+    so the two lines carry identical config dicts.  Uniform velocity meshes shard by
+    pencils (the fused step's items), AMR meshes by x-slabs; both split
+    the same global problem over the ranks (strong scaling)."""
+    if world == 1:
+        return "weak", "x-slab x1"
+    if CONFIGS[config]["levels"] == 0:
+        return "strong", f"pencils x{world}"
+    return "strong", f"x-slab x{world}"
+
+
+def config_dict(config, n_v, n_x, parallelism, world=1):
+    dofs = n_v * n_x
+    per_rank = dofs // max(world, 1)
+    return {"workload": NAMES[config], "config_id": config, "phase_dofs": dofs,
+            "velocity_dofs": n_v, "x_dofs": n_x, "bc": "absorbing", "dt": 0.1,
+            "parallelism": parallelism,
+            "l2": ("inputs larger than L2 (state %.2f GB per rank)" % (per_rank * 8 / 1e9)
+                   if per_rank * 8 > 126e6 else
+                   "state %.1f MB per rank fits in the 126 MB L2, not flushed: a latency/"
+                   "throughput figure, not an HBM-roofline one (SURVEY 8d)" % (per_rank * 8 / 1e6)),
+            "initial_data": "Landau f=(2pi)^-1.5 exp(-|v|^2/2)(1+0.01cos(0.5x))"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -148,28 +173,19 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfgd = dict(CONFIGS[args.config])
     cfg = sv.SimConfig(**cfgd, n_steps=args.steps)
-    scaling, parallelism = "weak", f"x-slab x{world}"
+    scaling, parallelism = parallelism_for(args.config, world)
     if world > 1:
         from paper_2603_19959_b200.shard import PencilShardedSimulation, ShardedSimulation
-        try:
-            # plans the fused step covers: pencil sharding, the same problem split over
-            # the ranks (strong scaling), partial sums are the only exchange
+        if parallelism.startswith("pencils"):
             sim = PencilShardedSimulation(cfg, rank, world)
-            scaling, parallelism = "strong", f"pencils x{world}"
-        except ValueError:
-            # weak scaling: every rank keeps the N=1 slab (N_x grows with the rank count)
-            cfgd["n_x"] = cfgd["n_x"] * world
-            cfg = sv.SimConfig(**cfgd, n_steps=args.steps)
+        else:
             sim = ShardedSimulation(cfg, rank, world)
     else:
         sim = sv.Simulation(cfg)
-    n_v, n_x_local = sim.f.shape
-    if scaling == "strong":   # every rank holds the whole state, advances 1/world of it
-        dofs_local = n_v * n_x_local // world
-        dofs_total = n_v * n_x_local
-    else:
-        dofs_local = n_v * n_x_local
-        dofs_total = dofs_local * world
+    n_v = sim.f.shape[0]
+    n_x_global = sim.xgrid.n_dofs
+    dofs_total = n_v * n_x_global
+    dofs_local = dofs_total // world   # pencils: a 1/world share of the items; slabs: ~1/world
     stream = torch.cuda.current_stream()
     rec = torch.empty(5, dtype=torch.float64, device=sim.f.device)
     lib = _capi.lib()
@@ -270,15 +286,7 @@ def run_ours(args):
         "metric": METRIC, "value": dofs_total / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": NAMES[args.config], "config_id": args.config,
-                   "phase_dofs": dofs_total, "velocity_dofs": n_v,
-                   "x_dofs": dofs_total // n_v, "bc": cfg.bc, "dt": cfg.dt,
-                   "parallelism": parallelism,
-                   "l2": ("inputs larger than L2 (state %.2f GB)" % (dofs_local * 8 / 1e9)
-                          if dofs_local * 8 > 126e6 else
-                          "state %.1f MB fits in the 126 MB L2, not flushed: a latency/throughput "
-                          "figure, not an HBM-roofline one (SURVEY 8d)" % (dofs_local * 8 / 1e6)),
-                   "initial_data": "Landau f=(2pi)^-1.5 exp(-|v|^2/2)(1+0.01cos(0.5x))"},
+        "config": config_dict(args.config, n_v, n_x_global, parallelism, world),
         "pipeline": ("one HBM pass per step: k_step_fused (v-sweep + trailing half-x + "
                      "moments + next leading half-x + rho), 16 B/DOF" if fused else
                      "v-sweep pass + fused X.X pass (moments, rho), 32 B/DOF"),
@@ -307,72 +315,52 @@ def run_ours(args):
         "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_sample(args.config, workers=1)
+        out["cpu_baseline"] = cpu_baseline_1core(args.config)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out))
 
 
-class CpuSample:
-    """Reference algorithm (oracle port) timed on a bounded sample of the workload.
-
-    The step is extrapolated from per-operator samples on the real state of the
-    config: the v-sweep on a subset of x columns (its cost is per column), the
-    x-advection on a subset of velocity rows (cost per row), and the full
-    rho + Poisson solve and diagnostics.  t_step = 2 t_x + t_field + t_v + t_diag.
-    """
+class CpuSteps:
+    """The reference algorithm (oracle/sldg_oracle.py, a numpy restatement of the reference
+    package, which is pure Python) stepping the FULL state of the config: each step is one
+    whole Strang step (half-x, rho + Poisson + E, v-sweep over every column, half-x,
+    diagnostics), timed by wall clock.  `workers` threads over columns / speed groups,
+    exactly like the reference's ThreadPoolExecutor (vsweep.py:436-440, xfield.py:101-103),
+    BLAS pinned to one thread (SURVEY.md §8(d) protocol)."""
 
     def __init__(self, config, workers):
         from oracle import sldg_oracle as so
-        self.so = so
         self.config = config
         self.workers = workers
         cfgd = CONFIGS[config]
         t0 = time.perf_counter()
         self.sim = so.Sim(dim=cfgd["dim"], n_base=cfgd["n_base"], levels=cfgd["levels"],
-                          degree=cfgd["degree"], n_x=cfgd["n_x"])
+                          degree=cfgd["degree"], n_x=cfgd["n_x"], workers=workers)
         self.setup_s = time.perf_counter() - t0
         self.n_v, self.n_x = self.sim.f.shape
-        self.kc = max(1, min(self.n_x, 8 * max(1, workers)))
-        self.kr = max(1, self.n_v // 8)
-        self.xp = so.x_plan(self.sim.xg, self.sim.vc[:self.kr, 0], 0.5 * self.sim.dt)
 
-    def sample(self):
+    def step(self):
         from threadpoolctl import threadpool_limits
-        so, sim = self.so, self.sim
-        with threadpool_limits(limits=1 if self.workers == 1 else None):
+        with threadpool_limits(limits=1):
             t0 = time.perf_counter()
-            e = sim.field_solve()
-            t_field = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            sim.diagnostics(e)
-            t_diag = time.perf_counter() - t0
-            cols = np.arange(self.kc)
-            fc = np.ascontiguousarray(sim.f[:, cols])
-            t0 = time.perf_counter()
-            so.advect_v(fc, e[cols], sim.dt, sim.plan, sim.bc, workers=self.workers)
-            t_v = (time.perf_counter() - t0) * self.n_x / self.kc
-            fr = np.ascontiguousarray(sim.f[:self.kr])
-            t0 = time.perf_counter()
-            so.advect_x(fr, self.xp, sim.xg.n_cells, workers=self.workers)
-            t_x = (time.perf_counter() - t0) * self.n_v / self.kr
-        t_step = 2 * t_x + t_field + t_v + t_diag
-        return {"value": self.n_v * self.n_x / t_step, "unit": UNIT, "cores": int(self.workers),
-                "kind": "port", "ms_per_step": t_step * 1e3,
-                "sample": f"oracle/sldg_oracle.py (reference algorithm, numpy) on the "
-                          f"{self.config} state: v-sweep on {self.kc}/{self.n_x} columns, "
-                          f"x-advect on {self.kr}/{self.n_v} rows (both scaled linearly), full "
-                          f"rho+Poisson and diagnostics; setup {self.setup_s:.1f}s excluded",
-                "breakdown_s": {"advect_x_half": t_x, "field": t_field, "advect_v": t_v,
-                                "diag": t_diag}}
+            self.sim.step()
+            return time.perf_counter() - t0
+
+    def describe(self, n_steps):
+        return (f"oracle/sldg_oracle.py (reference algorithm, numpy) Sim.step() on the full "
+                f"{self.config} state ({self.n_v} x {self.n_x}): {n_steps} whole Strang "
+                f"step(s), {self.workers} worker thread(s), BLAS 1 thread; setup "
+                f"{self.setup_s:.1f}s excluded")
 
 
-def cpu_sample(config, workers, reps=2):
-    cs = CpuSample(config, workers)
-    runs = [cs.sample() for _ in range(reps)]
-    best = min(runs, key=lambda r: r["ms_per_step"])
-    return best
+def cpu_baseline_1core(config):
+    """One full Strang step at 1 core (the GPU arm's cpu_baseline)."""
+    cs = CpuSteps(config, workers=1)
+    t = cs.step()
+    return {"value": cs.n_v * cs.n_x / t, "unit": UNIT, "cores": 1, "kind": "port",
+            "ms_per_step": t * 1e3, "sample": cs.describe(1)}
 
 
 def run_reference(args):
@@ -380,26 +368,36 @@ def run_reference(args):
     if rank != 0:
         return
     workers = os.cpu_count() or 1
-    cs = CpuSample(args.config, workers)
-    vals = []
-    last = None
+    t_start = time.perf_counter()
+    cs = CpuSteps(args.config, workers)
+    warm = args.warmup
+    times = []
     for k in range(args.warmup + args.steps):
-        last = cs.sample()
-        if k >= args.warmup:
-            vals.append(last["ms_per_step"])
-    ms = float(np.median(vals)) if vals else last["ms_per_step"]
+        t = cs.step()
+        if k == 0 and (args.warmup + args.steps) * t > args.cpu_budget:
+            # keep the whole run within a few minutes: the CPU needs no warm-up beyond
+            # the first step (no JIT, no clocks to ramp)
+            warm = 1
+        if k < warm:
+            continue
+        times.append(t)
+        if len(times) == args.steps:
+            break
+    t_wall = time.perf_counter() - t_start
+    ms = float(np.mean(times)) * 1e3
     dofs = cs.n_v * cs.n_x
     value = dofs / (ms * 1e-3)
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+    scaling, parallelism = parallelism_for(args.config, world)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": len(times),
+           "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": NAMES[args.config], "config_id": args.config,
-                      "phase_dofs": dofs, **CONFIGS[args.config]},
+           "config": config_dict(args.config, cs.n_v, cs.n_x, parallelism),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                            "sample": last["sample"]},
+                            "sample": cs.describe(len(times))},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
-                   "d2h_bytes_per_step": 0}}
+                   "d2h_bytes_per_step": 0},
+           "wall_s": t_wall, "timing": "wall clock per whole step, mean over the timed steps"}
     print(json.dumps(out))
 
 
@@ -412,7 +410,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-budget", type=float, default=240.0,
+                    help="reference arm: seconds for warm-up + timed steps before the "
+                         "warm-up is cut to one step")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

@@ -281,10 +281,15 @@ def _dedup_sorted(v, tol):
     return v[np.concatenate(([True], np.diff(v) > tol))]
 
 
-def make_pencils(mesh: Mesh, direction):
-    """CSR pencils along `direction`, weights 1/n_c (pencil.py:60-138)."""
+def make_pencils(mesh: Mesh, direction, weights="count"):
+    """CSR pencils along `direction`, weights 1/n_c (pencil.py:60-138).
+
+    weights="area" (not in the reference): each entry weighs the fraction
+    of the cell's transverse area its pencil covers, normalised per cell; 1.0 for cells in
+    a single pencil."""
     tol = 1e-9 * mesh.base_width
     tdims = [t for t in range(mesh.dim) if t != direction]
+    areas = []
     if tdims:
         ivs = []
         for t in tdims:
@@ -299,15 +304,25 @@ def make_pencils(mesh: Mesh, direction):
                        & (mesh.lo[:, t1] <= b2[0] + tol)
                        & (mesh.lo[:, t1] + mesh.width[:, t1] >= b2[1] - tol))
                 members.append(np.nonzero(hit)[0])
+                areas.append((b1[1] - b1[0]) * (b2[1] - b2[0]))
     else:
         members = [np.arange(mesh.n_cells)]
-    ids = [m[np.argsort(mesh.lo[m, direction], kind="stable")] for m in members]
+        areas = [1.0]
+    order = [np.argsort(mesh.lo[m, direction], kind="stable") for m in members]
+    ids = [m[o] for m, o in zip(members, order)]
     offsets = np.concatenate(([0], np.cumsum([len(m) for m in ids]))).astype(np.int64)
     cid = np.concatenate(ids)
     counts = np.bincount(cid, minlength=mesh.n_cells)
+    if weights == "area":
+        pa = np.repeat(np.array(areas), [len(m) for m in ids])
+        ca = (np.prod(mesh.width[cid][:, tdims], axis=1) if tdims else np.ones(len(cid)))
+        frac = pa / ca
+        tot = np.bincount(cid, weights=frac, minlength=mesh.n_cells)
+        w = np.where(counts[cid] == 1, 1.0, frac / tot[cid])
+    else:
+        w = 1.0 / counts[cid]
     return Pencils(direction, offsets, cid, mesh.lo[cid, direction].copy(),
-                   mesh.width[cid, direction].copy(), mesh.levels[cid].copy(),
-                   1.0 / counts[cid])
+                   mesh.width[cid, direction].copy(), mesh.levels[cid].copy(), w)
 
 
 def mark_conforming(ps: Pencils, bc):
@@ -722,11 +737,11 @@ class Sim:
 
     def __init__(self, dim=3, n_base=4, levels=0, radius=6.0, degree=3, n_x=64, degree_x=2,
                  wave_number=0.5, perturbation=0.01, dt=0.1, bc=ABSORBING, force_slow=False,
-                 mesh=None):
-        self.dt, self.bc, self.force_slow = dt, bc, force_slow
+                 mesh=None, pencil_weights="count", workers=1):
+        self.dt, self.bc, self.force_slow, self.workers = dt, bc, force_slow, workers
         self.basis = Basis(degree)
         self.mesh = mesh if mesh is not None else make_mesh(dim, n_base, levels, radius)
-        ps = mark_conforming(make_pencils(self.mesh, 0), bc)
+        ps = mark_conforming(make_pencils(self.mesh, 0, pencil_weights), bc)
         self.plan = make_plan(self.mesh, ps, degree)
         self.xg = XGrid(n_x, degree_x, 2.0 * np.pi / wave_number)
         self.vc = vcoords(self.mesh, self.basis)
@@ -747,10 +762,11 @@ class Sim:
                     e_field=ee, e_total=0.5 * m2 + ee)
 
     def step(self):
-        advect_x(self.f, self.xplan, self.xg.n_cells)
+        w = self.workers
+        advect_x(self.f, self.xplan, self.xg.n_cells, workers=w)
         e = self.field_solve()
-        advect_v(self.f, e, self.dt, self.plan, self.bc, self.force_slow)
-        advect_x(self.f, self.xplan, self.xg.n_cells)
+        advect_v(self.f, e, self.dt, self.plan, self.bc, self.force_slow, workers=w)
+        advect_x(self.f, self.xplan, self.xg.n_cells, workers=w)
         self.t += self.dt
         return self.diagnostics(e)
 

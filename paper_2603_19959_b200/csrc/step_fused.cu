@@ -686,7 +686,8 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
     const size_t R = (size_t)lg * OV;
     const size_t tables = 2 * sizeof(double) * (nmax + 3 * R * nmax + (nmax * OV + 1) / 2);
     const size_t smem = sizeof(double) * (kFRing * R * n_cols + 2 * R * g.rw) + fixed + tables;
-    const size_t red = sizeof(double) * std::max<size_t>(OV * n_cols, 3 * threads);
+    // the moment reduction stores 3 values per launched thread (blockDim rounded to 32)
+    const size_t red = sizeof(double) * std::max<size_t>(OV * n_cols, 3 * ((threads + 31) / 32 * 32));
     if (smem <= budget && sizeof(double) * 2 * R * g.rw >= red) {
       // prefer two CTAs per SM when possible
       if (2 * smem <= budget || g.lg == 0) {
@@ -734,7 +735,7 @@ static FusedKernel pick_kernel(int lg, long long n_xc, int mode) {
 }
 
 static FusedKernel fused_kernel(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
-                                int mode = 0) {
+                                int mode) {
   switch (vp->o * 10 + xp->o) {
 #define CASE(A, B) \
   case A * 10 + B: return pick_kernel<A, B>(g.lg, xp->n_cells, mode);
@@ -745,11 +746,23 @@ static FusedKernel fused_kernel(const sldg_vplan* vp, const sldg_xplan* xp, cons
   return nullptr;
 }
 
-// resident persistent grid (deterministic for a device): partial rows written
-static int fused_grid(FusedKernel k, const FusedGeom& g, long long* grid) {
-  int per_sm = 0;
-  SLDG_CUDA_TRY(resident_ctas((const void*)k, g.threads, (int)g.smem, &per_sm));
-  *grid = std::max<long long>(1, std::min<long long>(g.grid, (long long)std::max(per_sm, 1) * sm_count()));
+// resident persistent grid (deterministic for a device): one grid for all three
+// modes, the smallest of their resident counts, so that the folds (which only know
+// the plan) read exactly the partial rows any mode's launch wrote
+static int fused_grid(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g,
+                      long long* grid) {
+  int per_sm = 1 << 30;
+  for (int mode = 0; mode < 3; ++mode) {
+    FusedKernel k = fused_kernel(vp, xp, g, mode);
+    if (!k) {
+      set_error("fused step: no kernel for this degree / line group");
+      return SLDG_ERR_UNSUPPORTED;
+    }
+    int r = 0;
+    SLDG_CUDA_TRY(resident_ctas((const void*)k, g.threads, (int)g.smem, &r));
+    per_sm = std::min(per_sm, std::max(r, 1));
+  }
+  *grid = std::max<long long>(1, std::min<long long>(g.grid, (long long)per_sm * sm_count()));
   return SLDG_OK;
 }
 
@@ -982,7 +995,7 @@ int launch_step(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g, 
     set_error("fused step: no kernel for this degree / line group");
     return SLDG_ERR_UNSUPPORTED;
   }
-  int rc = fused_grid(k, g, grid);
+  int rc = fused_grid(vp, xp, g, grid);
   if (rc) return rc;
   SLDG_CUDA_TRY(launch_pdl(k, dim3((unsigned)*grid), dim3(g.threads), g.smem, st, vp->dev,
                            xp->dev, fin, fout, (int)n_cols, (int)xp->n_cells, speeds, (int)bc,
@@ -1025,7 +1038,7 @@ int sldg_step_fused_advice(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n
   FusedGeom g;
   int rc = check_geom(vp, xp, n_cols, ld, &g);
   if (rc) return rc;
-  FusedKernel k = fused_kernel(vp, xp, g);
+  FusedKernel k = fused_kernel(vp, xp, g, 0);
   if (!k) {
     set_error("fused step: no kernel for this degree / line group");
     return SLDG_ERR_UNSUPPORTED;
@@ -1120,13 +1133,13 @@ int sldg_step_fused_fold(const sldg_vplan* vp, const sldg_xplan* xp, int64_t n_c
   FusedGeom g;
   int rc = check_geom(vp, xp, n_cols, ld, &g);
   if (rc) return rc;
-  FusedKernel k = fused_kernel(vp, xp, g);
+  FusedKernel k = fused_kernel(vp, xp, g, 0);
   if (!k) {
     set_error("fused step: no kernel for this degree / line group");
     return SLDG_ERR_UNSUPPORTED;
   }
   long long grid = 0;
-  rc = fused_grid(k, g, &grid);
+  rc = fused_grid(vp, xp, g, &grid);
   if (rc) return rc;
   const FusedScratch s = fused_scratch(vp, g, n_cols, scratch);
   cudaStream_t st = (cudaStream_t)stream;
@@ -1157,12 +1170,12 @@ int sldg_field_chain(const sldg_vplan* vp, const sldg_xplan* xp, const sldg_pois
   const FusedScratch s = fused_scratch(vp, g, n_cols, scratch);
   long long grid = 0;
   if (!rho_in) {   // partials of the previous sldg_step_fused_deferred
-    FusedKernel k = fused_kernel(vp, xp, g);
+    FusedKernel k = fused_kernel(vp, xp, g, 0);
     if (!k) {
       set_error("fused step: no kernel for this degree / line group");
       return SLDG_ERR_UNSUPPORTED;
     }
-    rc = fused_grid(k, g, &grid);
+    rc = fused_grid(vp, xp, g, &grid);
     if (rc) return rc;
   }
   cudaStream_t st = (cudaStream_t)stream;

@@ -48,8 +48,21 @@ def _edges(vals, tol):
     return vals[np.concatenate(([True], np.diff(vals) > tol))]
 
 
-def extract_pencils(mesh: VelocityMesh, direction: int) -> PencilSet:
-    """Pencil decomposition along `direction` (pencil.py:60-138)."""
+WEIGHT_MODES = ("count", "area")
+
+
+def extract_pencils(mesh: VelocityMesh, direction: int, weights: str = "count") -> PencilSet:
+    """Pencil decomposition along `direction` (pencil.py:60-138).
+
+    weights="count" (default) gives the reference's entry weights 1/n_c, n_c the number of
+    pencils cell c lies in (pencil.py:124,137).  weights="area" gives each entry the
+    fraction of the cell's transverse area that the pencil covers, normalised per cell:
+    with two AMR levels a coarse cell can be cut into transverse intervals of unequal
+    width, where 1/n_c is not mass conservative and the area fractions are (SURVEY.md
+    §8 N1).  Cells in one pencil have weight 1.0 in both modes.
+    """
+    if weights not in WEIGHT_MODES:
+        raise PencilError(f"weights must be one of {WEIGHT_MODES}, got {weights!r}")
     if not 0 <= direction < mesh.dim:
         raise PencilError(f"direction must be in [0, {mesh.dim}), got {direction}")
     tol = 1e-9 * mesh.base_width
@@ -58,6 +71,7 @@ def extract_pencils(mesh: VelocityMesh, direction: int) -> PencilSet:
     if tdims:
         ranges = []
         n_iv = []
+        edges = []
         for t in tdims:
             e = _edges(np.concatenate([mesh.lo[:, t], mesh.lo[:, t] + mesh.width[:, t]]), tol)
             lo_t, hi_t = mesh.lo[:, t], mesh.lo[:, t] + mesh.width[:, t]
@@ -66,6 +80,7 @@ def extract_pencils(mesh: VelocityMesh, direction: int) -> PencilSet:
             k1 = np.searchsorted(e, hi_t + tol, side="right") - 1   # exclusive interval bound
             ranges.append((k0, k1))
             n_iv.append(len(e) - 1)
+            edges.append(e)
         (a0, b0), (a1, b1) = ranges
         c0, c1 = np.maximum(b0 - a0, 0), np.maximum(b1 - a1, 0)
         cnt = c0 * c1
@@ -75,12 +90,16 @@ def extract_pencils(mesh: VelocityMesh, direction: int) -> PencilSet:
         i1 = a1[cell] + local // c0[cell]
         pencil = i1 * n_iv[0] + i0
         n_pencils = n_iv[0] * n_iv[1]
+        # transverse area of the pencil / transverse area of the cell
+        frac = ((edges[0][i0 + 1] - edges[0][i0]) * (edges[1][i1 + 1] - edges[1][i1])
+                / (mesh.width[cell, tdims[0]] * mesh.width[cell, tdims[1]]))
     else:
         cell = np.arange(n)
         pencil = np.zeros(n, dtype=np.int64)
         n_pencils = 1
+        frac = np.ones(n)
     order = np.lexsort((cell, mesh.lo[cell, direction], pencil))
-    cell, pencil = cell[order], pencil[order]
+    cell, pencil, frac = cell[order], pencil[order], frac[order]
     counts_p = np.bincount(pencil, minlength=n_pencils)
     if (counts_p == 0).any():
         q = int(np.nonzero(counts_p == 0)[0][0])
@@ -107,9 +126,14 @@ def extract_pencils(mesh: VelocityMesh, direction: int) -> PencilSet:
     if (counts == 0).any():
         missing = int(np.nonzero(counts == 0)[0][0])
         raise PencilError(f"cell {missing} appears in no pencil of direction {direction}")
+    if weights == "area":
+        total = np.bincount(cell, weights=frac, minlength=n)
+        wts = np.where(counts[cell] == 1, 1.0, frac / total[cell])
+    else:
+        wts = 1.0 / counts[cell]
     return PencilSet(direction=direction, n_pencils=int(n_pencils), offsets=offsets,
                      cell_ids=cell.astype(np.int64), lowers=lo.copy(), widths=w.copy(),
-                     levels=mesh.levels[cell].copy(), weights=1.0 / counts[cell])
+                     levels=mesh.levels[cell].copy(), weights=wts)
 
 
 def classify_conforming(pset: PencilSet, mesh: VelocityMesh, bc: str = "absorbing") -> PencilSet:

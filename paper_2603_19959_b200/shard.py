@@ -198,7 +198,8 @@ class ShardedSimulation:
         self.basis = DGBasis(c.degree)
         self.mesh = mesh if mesh is not None else build_mesh(c.dim, c.n_base, c.levels, c.radius)
         self.perm = build_permutation(self.basis, c.dim)
-        pset = classify_conforming(extract_pencils(self.mesh, 0), self.mesh, c.bc)
+        pset = classify_conforming(extract_pencils(self.mesh, 0, c.pencil_weights), self.mesh,
+                                   c.bc)
         self.sweep_plan = build_sweep_plan(self.mesh, pset, self.perm, self.basis)
         self.xgrid = XGrid(c.n_x, c.degree_x, c.length)
         self.vcoords = velocity_dof_coords(self.mesh, self.basis, self.perm)
@@ -476,3 +477,17 @@ class PencilShardedSimulation(Simulation):
         table = self.advance(1)
         self.t += self.config.dt
         return self._record(self.t, table[0])
+
+    def run(self):
+        raise NotImplementedError("PencilShardedSimulation: use advance()/step(); run() "
+                                  "needs the global t=0 diagnostics of all ranks' rows")
+
+    # Simulation methods that act on the whole buffer: on a sharded rank the rows of the
+    # other ranks are stale, so these would return plausible but wrong physics.
+    def _whole_buffer_only(self, *_a, **_k):
+        raise NotImplementedError("PencilShardedSimulation: only advance()/step() are valid on "
+                                  "a sharded rank (rows of other ranks are not current); "
+                                  "read this rank's rows with owned_rows()")
+
+    enqueue_step = step_host = field_solve = diagnostics = advance_graph = _whole_buffer_only
+    _lead_x_rho = _xx = _trail_x_mom = _advect_x = _advect_v = _field = _whole_buffer_only

@@ -73,6 +73,36 @@ class _PencilGroup:
     def simple(self) -> bool:
         return bool((self.cell_weights == 1.0).all())
 
+    # the reference's copy / accumulate partition of the flat positions (vsweep.py:285-291,
+    # 366-383); the device plan carries the same information as its target CSR
+    @property
+    def flat_weights(self) -> np.ndarray:
+        o = self._lines.shape[1]
+        w = np.broadcast_to(self.cell_weights[:, None, :, None],
+                            (self.cell_weights.shape[0], self._lines.shape[0],
+                             self.n_cells, o))
+        return np.ascontiguousarray(w).reshape(self.n_lines, self.n_cells * o)
+
+    @property
+    def copy_pos(self) -> np.ndarray:
+        return np.nonzero(self.flat_weights.ravel() == 1.0)[0]
+
+    @property
+    def copy_targets(self) -> np.ndarray:
+        return self.gather.ravel()[self.copy_pos]
+
+    @property
+    def acc_pos(self) -> np.ndarray:
+        return np.nonzero(self.flat_weights.ravel() != 1.0)[0]
+
+    @property
+    def acc_targets(self) -> np.ndarray:
+        return self.gather.ravel()[self.acc_pos]
+
+    @property
+    def acc_weights(self) -> np.ndarray:
+        return self.flat_weights.ravel()[self.acc_pos]
+
 
 class SweepPlan:
     """Static plan for one sweep direction (vsweep.py:294-304) + its device image."""

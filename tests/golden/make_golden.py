@@ -181,6 +181,26 @@ def xside():
     save("xside.npz", **out)
 
 
+def poisson_large():
+    """Poisson solve + E at the x resolutions of configs 4 and 5 (N_x = 128, 256, 512): the
+    device path applies the leading block of the augmented system's inverse, the reference
+    LU (xfield.py:146,163); both are ~3e-13 from the exact solution of the discrete system
+    at N_x = 512."""
+    out = {}
+    rng = np.random.default_rng(512)
+    for nx in (128, 256, 512):
+        xg = sv.XGrid(nx, 2, 4.0 * np.pi)
+        ps = sv.PoissonSolver(xg)
+        x = xg.dof_coords
+        for k, eps in enumerate((0.01, 0.3)):
+            rho = 1.0 + eps * np.cos(0.5 * x) + 0.02 * np.sin(1.5 * x) + 1e-4 * rng.random(x.size)
+            phi = ps.solve(rho)
+            out[f"nx{nx}_{k}_rho"] = rho
+            out[f"nx{nx}_{k}_phi"] = phi
+            out[f"nx{nx}_{k}_E"] = ps.electric_field(phi)
+    save("poisson.npz", **out)
+
+
 def simulations():
     """Short Strang runs: diagnostics per step + sampled coefficients."""
     out = {}
@@ -211,7 +231,7 @@ def simulations():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["basis", "meshes", "sweeps", "x", "sim"]
+    which = sys.argv[1:] or ["basis", "meshes", "sweeps", "x", "poisson", "sim"]
     if "basis" in which:
         basis_and_1d()
     if "meshes" in which:
@@ -220,5 +240,7 @@ if __name__ == "__main__":
         sweeps()
     if "x" in which:
         xside()
+    if "poisson" in which:
+        poisson_large()
     if "sim" in which:
         simulations()

@@ -165,3 +165,30 @@ def test_dump_pencils_and_shifted_source(tmp_path):
         for i in range(5):
             assert np.array_equal(per[:, i], v[:, (i - k) % 5])
             assert np.array_equal(ab[:, i], v[:, i - k] if 0 <= i - k < 5 else 0 * v[:, i])
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference package not present")
+@pytest.mark.parametrize("nb,lv,p", [(4, 2, 3), (3, 1, 2), (4, 1, 2)])
+def test_pencil_group_partitions_match_reference(nb, lv, p):
+    """_PencilGroup copy_pos / copy_targets / acc_pos / acc_targets / acc_weights equal the
+    reference's (vsweep.py:285-291, 366-383), in both bcs."""
+    import sys
+    if REF_SRC not in sys.path:
+        sys.path.append(REF_SRC)
+    import sldg_vlasov as ref
+    for bc in ("absorbing", "periodic"):
+        m = ref.build_mesh(3, nb, lv, 6.0)
+        b = ref.DGBasis(p)
+        rp = ref.build_sweep_plan(m, ref.classify_conforming(ref.extract_pencils(m, 0), m, bc),
+                                  ref.build_permutation(b, 3), b)
+        m2 = sv.build_mesh(3, nb, lv, 6.0)
+        b2 = sv.DGBasis(p)
+        op = sv.build_sweep_plan(m2, sv.classify_conforming(sv.extract_pencils(m2, 0), m2, bc),
+                                 sv.build_permutation(b2, 3), b2)
+        assert len(rp.groups) == len(op.groups)
+        for g, h in zip(rp.groups, op.groups):
+            for k in ("copy_pos", "copy_targets", "acc_pos", "acc_targets", "acc_weights"):
+                np.testing.assert_array_equal(getattr(g, k), getattr(h, k))

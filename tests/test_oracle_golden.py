@@ -175,3 +175,47 @@ def test_fit_oracle():
     assert rate is not None and abs(rate + 0.1533) <= 1e-3
     rate, npk = so.peak_run_fit(t, np.exp(-0.2 * t))
     assert rate is None and npk < 2
+
+
+def test_poisson_large_nx(golden):
+    """N_x = 128 / 256 / 512 Poisson + E (configs 4 and 5) against the reference."""
+    g = golden("poisson.npz")
+    for nx in (128, 256, 512):
+        ps = so.Poisson(so.XGrid(nx, 2, 4.0 * np.pi))
+        for k in range(2):
+            phi = ps.solve(g[f"nx{nx}_{k}_rho"])
+            np.testing.assert_allclose(phi, g[f"nx{nx}_{k}_phi"], rtol=0,
+                                       atol=1e-14 * np.abs(g[f"nx{nx}_{k}_phi"]).max())
+            e = ps.efield(phi)
+            np.testing.assert_allclose(e, g[f"nx{nx}_{k}_E"], rtol=0,
+                                       atol=1e-14 * np.abs(g[f"nx{nx}_{k}_E"]).max())
+
+
+def test_coefficient_goldens_consistent(golden):
+    """The multi-step reference runs (coeffs_*.npz) carry the records of run_*.npz."""
+    import os
+    for name in ("cfg1", "cfg3", "cfg4", "cfg2"):
+        path = os.path.join(os.path.dirname(__file__), "golden", f"coeffs_{name}.npz")
+        if not os.path.exists(path):
+            continue
+        c = golden(f"coeffs_{name}.npz")
+        r = golden(f"run_{name}.npz")
+        np.testing.assert_allclose(c["records"][:, 2], r["records"][:, 2], rtol=1e-12)
+        assert c["records"].shape == r["records"].shape
+
+
+@pytest.mark.parametrize("nb,lv", [(4, 2), (3, 2), (5, 2), (4, 1)])
+def test_area_weights_product_equals_oracle(nb, lv):
+    """weights="area": the product's vectorised builder and the oracle's
+    per-pencil scan give identical weights, and every cell's weights sum to one."""
+    import paper_2603_19959_b200 as sv
+    m = sv.build_mesh(3, nb, lv, 6.0)
+    ps = sv.extract_pencils(m, 0, "area")
+    om = so.make_mesh(3, nb, lv, 6.0)
+    ops = so.make_pencils(om, 0, "area")
+    np.testing.assert_array_equal(ps.cell_ids, ops.cell_ids)
+    np.testing.assert_array_equal(ps.weights, ops.weights)
+    tot = np.bincount(ps.cell_ids, weights=ps.weights)
+    assert np.abs(tot - 1.0).max() <= 4.5e-16
+    cnt = sv.extract_pencils(m, 0)
+    np.testing.assert_array_equal(ps.weights == 1.0, cnt.weights == 1.0)
