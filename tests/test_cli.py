@@ -4,7 +4,8 @@ import json
 import numpy as np
 import pytest
 
-from paper_2603_19959_b200.cli import (CSV_HEADER, EXIT_CONFIG, EXIT_OK, TABLE2_PRESETS, main,
+from paper_2603_19959_b200.cli import (CSV_HEADER, EXIT_CONFIG, EXIT_NO_PEAKS, EXIT_OK,
+                                       TABLE2_PRESETS, main,
                                        parse_config)
 
 
@@ -40,3 +41,81 @@ def test_run_writes_outputs(tmp_path, capsys):
     assert abs(data[0, 1] - 0.02) < 1e-3
     assert json.loads(summ.read_text())["cells"] == 16
     assert "semilogy" in plot.read_text()
+
+
+# The reference CLI suite's behaviours on the GPU run (pkg/tests/test_cli.py:55-141):
+# %.17e CSV cells, per-step mass column with periodic bc, byte-identical reruns, the
+# "---" sentinel with exit 4 when fewer than two peaks exist, exit 3 on an unwritable path.
+SHORT = ["--dv", "1", "--Nb", "16", "--p", "2", "--Nx", "16", "--steps", "3"]
+
+
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_flags_parse_on_cpu():
+    cfg, ns = parse_config(["--force-slow-path", "--workers", "3", "--dv", "1", "--bc",
+                            "periodic", "--summary", "x.json"])
+    assert cfg.force_slow and cfg.workers == 3 and cfg.dim == 1 and cfg.bc == "periodic"
+    assert ns.summary == "x.json"
+
+
+@pytest.mark.gpu
+def test_csv_cells_are_17_digit_scientific(tmp_path, capsys):
+    _gpu()
+    csv = tmp_path / "c.csv"
+    assert main(SHORT[:-1] + ["40", "--csv", str(csv), "--plot-script",
+                              str(tmp_path / "p.py")]) in (EXIT_OK, EXIT_NO_PEAKS)
+    capsys.readouterr()
+    lines = csv.read_text().splitlines()
+    assert float(lines[1].split(",")[0]) == 0.0
+    for line in lines[1:3]:
+        for tok in line.split(","):
+            assert len(tok.split("e")[0].split(".")[1]) == 17
+
+
+@pytest.mark.gpu
+def test_periodic_mass_column_constant(tmp_path, capsys):
+    _gpu()
+    csv = tmp_path / "m.csv"
+    assert main(SHORT[:-1] + ["60", "--bc", "periodic", "--csv", str(csv), "--plot-script",
+                              str(tmp_path / "p.py")]) == EXIT_OK
+    capsys.readouterr()
+    m0 = np.genfromtxt(csv, delimiter=",", names=True)["m0"]
+    assert np.abs(m0 - m0[0]).max() <= 1e-11 * abs(m0[0])
+
+
+@pytest.mark.gpu
+def test_rerun_writes_identical_bytes(tmp_path, capsys):
+    _gpu()
+    paths = [tmp_path / "r1.csv", tmp_path / "r2.csv"]
+    for p in paths:
+        assert main(SHORT + ["--csv", str(p), "--plot-script", str(tmp_path / "p.py")]) in (
+            EXIT_OK, EXIT_NO_PEAKS)
+    capsys.readouterr()
+    assert paths[0].read_bytes() == paths[1].read_bytes()
+
+
+@pytest.mark.gpu
+def test_too_few_peaks_gives_sentinel_and_exit_4(tmp_path, capsys):
+    _gpu()
+    from paper_2603_19959_b200.cli import EXIT_NO_PEAKS as NOPK
+    summ = tmp_path / "s.json"
+    code = main(SHORT + ["--csv", str(tmp_path / "s.csv"), "--plot-script",
+                         str(tmp_path / "p.py"), "--summary", str(summ)])
+    capsys.readouterr()
+    assert code == NOPK == 4
+    d = json.loads(summ.read_text())
+    assert d["gamma"] == "---" and d["rate_error_pct"] == "---"
+    assert (tmp_path / "s.csv").exists()
+
+
+@pytest.mark.gpu
+def test_unwritable_output_exits_3(tmp_path, capsys):
+    _gpu()
+    code = main(SHORT + ["--csv", str(tmp_path / "missing" / "dir" / "x.csv"),
+                         "--plot-script", str(tmp_path / "p.py")])
+    capsys.readouterr()
+    assert code == 3
