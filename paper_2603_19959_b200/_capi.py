@@ -12,7 +12,10 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libsldg.so")
+# SLDG_LIB_VARIANT=<name> loads _lib/libsldg_<name>.so instead (same-box A/B timing of
+# kernel variants, tools/ab_build.sh); the in-tree library otherwise
+LIB_PATH = os.path.join(_HERE, "_lib", "libsldg.so" if not os.environ.get("SLDG_LIB_VARIANT")
+                        else f"libsldg_{os.environ['SLDG_LIB_VARIANT']}.so")
 
 SLDG_OK = 0
 SLDG_ERR_ARG = 1

@@ -1,0 +1,20 @@
+#!/bin/bash
+# Build libsldg from the step_fused.cu of git revision $1 as _lib/libsldg_$2.so (the rest of
+# the sources from the working tree), for same-box A/B timing: SLDG_LIB_VARIANT=$2.
+set -e
+cd "$(dirname "$0")/.."
+rev=$1; name=$2
+tmp=$(mktemp -d)
+cp -r paper_2603_19959_b200/csrc/. "$tmp/"
+git show "$rev:paper_2603_19959_b200/csrc/step_fused.cu" > "$tmp/step_fused.cu"
+objs=()
+for f in "$tmp"/*.cu; do
+  o="$tmp/$(basename "$f").o"
+  nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC \
+    -Xcompiler -O3 --expt-relaxed-constexpr -Iinclude -I"$tmp" -c "$f" -o "$o" 2>/dev/null &
+  objs+=("$o")
+done
+wait
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o paper_2603_19959_b200/_lib/libsldg_$name.so "${objs[@]}"
+rm -rf "$tmp"
+echo built paper_2603_19959_b200/_lib/libsldg_$name.so
