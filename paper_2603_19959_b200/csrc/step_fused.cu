@@ -43,6 +43,8 @@
 #include <string>
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "plans.cuh"
 #include "sldg_common.cuh"
 #include "tma_util.cuh"
@@ -819,13 +821,34 @@ static FusedScratch fused_scratch(const sldg_vplan* vp, const FusedGeom& g, long
   return s;
 }
 
-// The field work between two fused steps in one single-CTA launch (1024
-// threads), each stage with the same per-element arithmetic and reduction order
-// as its stand-alone kernel, so the results are bitwise identical:
-//   [k_fold_cols, k_fold3] -> k_poisson_rhs -> k_gemv -> k_efield ->
-//   k_field_diag, k_level_mats.
+// The field work between two fused steps in one launch of a cluster of kChainCtas CTAs
+// (distributed shared memory between them), each stage with the same per-element
+// arithmetic and reduction order as its stand-alone kernel, so the results are bitwise
+// identical to  [k_fold_cols, k_fold3] -> k_poisson_rhs -> k_gemv -> k_efield ->
+// k_field_diag, k_level_mats:
+//   fold     CTA r folds its contiguous share of the columns (warp per column, lanes over
+//            the CTA partials, xor butterfly: k_fold_cols), CTA 0 the moments (k_fold3);
+//   rho      gathered from the cluster's shared memory into every CTA;
+//   rhs      rbar by the 1024-slot tree of k_poisson_rhs, the load vector b (every CTA);
+//   phi      rows split over the CTAs (warp per row, k_gemv), gathered;
+//   E        DOFs split over the CTAs (k_efield); CTA 0 gathers E for the diagnostics
+//            (the 1024-slot trees of k_field_diag) while every CTA forms the level
+//            matrices of its columns, one thread per (level, column, A|B).
+constexpr int kChainCtas = 8;
+constexpr int kChainThreads = 512;
+constexpr int kChainMaxDofs = 1024;   // x DOFs (and FE nodes) a chain handles
+
+// the 1024-slot tree of the stand-alone reductions, emulated with blockDim threads
+__device__ __forceinline__ double tree1024_sum(double* red) {
+  for (int st = 512; st > 0; st >>= 1) {
+    for (int t = threadIdx.x; t < st; t += blockDim.x) red[t] += red[t + st];
+    __syncthreads();
+  }
+  return red[0];
+}
+
 template <int O>
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __cluster_dims__(kChainCtas, 1, 1) __launch_bounds__(kChainThreads, 1)
 k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_part,
               const double* __restrict__ mom_part, long long n_parts,
               double* __restrict__ mom_prev, double* __restrict__ rho, const double* __restrict__ pxw,
@@ -835,133 +858,175 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
               DevBasis vb, double dt, double base_width, int n_levels,
               long long* __restrict__ lm_ns, double* __restrict__ lm_frac,
               double* __restrict__ lm_mats) {
-  constexpr int CH = 80;   // fsm: 32 x (CH + 1) doubles, b of the GEMV when it fits
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double r_s[kChainMaxDofs], phi_s[kChainMaxDofs], e_s[kChainMaxDofs];
   __shared__ double red[1024], red2[1024];
-  __shared__ double fsm[32 * (CH + 1)];
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, nw = blockDim.x >> 5;
+  const int rank = (int)cluster.block_rank();
   const int o = p + 1;
-  const long long n_dofs = n_cells * o, n_nodes = n_cells * p;
-  const int nd = (int)n_dofs, np = (int)n_parts;
+  const int nd = (int)(n_cells * o), nn = (int)(n_cells * p), np = (int)n_parts;
+  auto share = [&](int n, int r) { return (int)((long long)n * r / kChainCtas); };
+  const int c0 = share(nd, rank), c1 = share(nd, rank + 1);     // my columns / DOFs
+  const int q0 = share(nn, rank), q1 = share(nn, rank + 1);     // my FE rows
   // PDL: wait for the preceding fused step (its partials and state are complete),
   // then let the next fused step start its E-independent prologue alongside us
   grid_dep_wait();
   grid_dep_launch();
-  const double* r = rho_in;
-  if (!r) {
-    // fold the previous fused step's partials in k_fold_cols' order (lane l sums
-    // parts l, l+32, ...; then the xor butterfly): a warp per column, its partials
-    // contiguous (column-major), every warp's loads in flight at once
-    for (int c = wp; c < nd; c += nw) {
+  if (!rho_in) {
+    for (int c = c0 + wp; c < c1; c += nw) {
       const double* q = rho_part + (size_t)c * np;
-      double s = 0.0;
+      double sacc = 0.0;
 #pragma unroll 4
-      for (int k = lane; k < np; k += 32) s += __ldg(q + k);
+      for (int k = lane; k < np; k += 32) sacc += __ldg(q + k);
 #pragma unroll
-      for (int of = 16; of > 0; of >>= 1) s += __shfl_xor_sync(0xffffffffu, s, of);
-      if (lane == 0) rho[c] = s;
+      for (int of = 16; of > 0; of >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, of);
+      if (lane == 0) {
+        rho[c] = sacc;
+        r_s[c] = sacc;
+      }
     }
-    if (mom_prev && wp < 3) {
-      double s = 0.0;
-      for (long long k = lane; k < n_parts; k += 32) s += mom_part[k * 3 + wp];
+    if (rank == 0 && mom_prev && wp < 3) {
+      double sacc = 0.0;
+      for (long long k = lane; k < n_parts; k += 32) sacc += mom_part[k * 3 + wp];
 #pragma unroll
-      for (int of = 16; of > 0; of >>= 1) s += __shfl_xor_sync(0xffffffffu, s, of);
-      if (lane == 0) mom_prev[wp] = s;
+      for (int of = 16; of > 0; of >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, of);
+      if (lane == 0) mom_prev[wp] = sacc;
     }
-    __syncthreads();
-    r = rho;
+    cluster.sync();
+    for (int c = tid; c < nd; c += blockDim.x) {
+      if (c >= c0 && c < c1) continue;
+      int owner = 0;
+      while (c >= share(nd, owner + 1)) ++owner;
+      r_s[c] = *cluster.map_shared_rank(&r_s[c], owner);
+    }
+  } else {
+    for (int c = tid; c < nd; c += blockDim.x) r_s[c] = rho_in[c];
   }
-  // Poisson right-hand side (k_poisson_rhs)
-  double s = 0.0;
-  for (long long k = tid; k < n_dofs; k += blockDim.x) s = fma(pxw[k], r[k], s);
-  red[tid] = s;
+  // Poisson right-hand side (k_poisson_rhs): fma(w, r, 0) per slot, 1024-slot tree
+  for (int t = tid; t < 1024; t += blockDim.x) red[t] = t < nd ? fma(pxw[t], r_s[t], 0.0) : 0.0;
   __syncthreads();
-  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-    if (tid < st) red[tid] += red[tid + st];
-    __syncthreads();
-  }
-  const double rbar = red[0] / length;
-  for (long long node = tid; node < n_nodes; node += blockDim.x) {
-    const long long cell = node / p;
-    const int j = (int)(node - cell * p);
+  const double rbar = tree1024_sum(red) / length;
+  for (int node = tid; node < nn; node += blockDim.x) {
+    const int cell = node / p, j = node - cell * p;
     double v;
     if (j == 0) {
-      const long long kprev = (cell == 0 ? n_cells - 1 : cell - 1) * o + p;
-      const long long kthis = cell * o;
-      const double cprev = __dmul_rn(pxw[kprev], __dsub_rn(r[kprev], rbar));
-      const double cthis = __dmul_rn(pxw[kthis], __dsub_rn(r[kthis], rbar));
+      const int kprev = (cell == 0 ? (int)n_cells - 1 : cell - 1) * o + p, kthis = cell * o;
+      const double cprev = __dmul_rn(pxw[kprev], __dsub_rn(r_s[kprev], rbar));
+      const double cthis = __dmul_rn(pxw[kthis], __dsub_rn(r_s[kthis], rbar));
       v = (cell == 0) ? __dadd_rn(cthis, cprev) : __dadd_rn(cprev, cthis);
     } else {
-      const long long k = cell * o + j;
-      v = __dmul_rn(pxw[k], __dsub_rn(r[k], rbar));
+      const int k = cell * o + j;
+      v = __dmul_rn(pxw[k], __dsub_rn(r_s[k], rbar));
     }
-    b[node] = v;
-    if (n_nodes <= 32 * (CH + 1)) fsm[node] = v;   // b staged in shared memory for the GEMV
+    phi_s[node] = v;   // b, staged for the GEMV
+    if (rank == 0) b[node] = v;
   }
   __syncthreads();
-  // phi = G b (k_gemv: warp per row)
-  const int nn = (int)n_nodes;
-  const double* bsrc = nn <= 32 * (CH + 1) ? fsm : b;
-  for (int row = wp; row < nn; row += nw) {
+  // phi = G b (k_gemv: warp per row), my rows; b lives in phi_s until the rows are done
+  double rowv[kChainMaxDofs / (kChainCtas * 16) + 1];
+  int nrow = 0;
+  for (int row = q0 + wp; row < q1; row += nw) {
     double t = 0.0;
     const double* g = green + (size_t)row * nn;
 #pragma unroll 4
-    for (int k = lane; k < nn; k += 32) t = fma(__ldg(g + k), bsrc[k], t);
+    for (int k = lane; k < nn; k += 32) t = fma(__ldg(g + k), phi_s[k], t);
 #pragma unroll
     for (int of = 16; of > 0; of >>= 1) t += __shfl_xor_sync(0xffffffffu, t, of);
-    if (lane == 0) phi[row] = t;
+    rowv[nrow++] = t;
   }
   __syncthreads();
-  // E (k_efield)
+  nrow = 0;
+  for (int row = q0 + wp; row < q1; row += nw) {
+    const double t = rowv[nrow++];
+    if (lane == 0) {
+      phi_s[row] = t;
+      phi[row] = t;
+    }
+  }
+  cluster.sync();
+  for (int node = tid; node < nn; node += blockDim.x) {
+    if (node >= q0 && node < q1) continue;
+    int owner = 0;
+    while (node >= share(nn, owner + 1)) ++owner;
+    red2[node] = *cluster.map_shared_rank(&phi_s[node], owner);
+  }
+  __syncthreads();
+  for (int node = tid; node < nn; node += blockDim.x)
+    if (node < q0 || node >= q1) phi_s[node] = red2[node];
+  __syncthreads();
+  // E (k_efield), my DOFs
   const double sc = -(2.0 / h);
-  for (long long k = tid; k < n_dofs; k += blockDim.x) {
-    const long long cell = k / o;
-    const int i = (int)(k - cell * o);
+  for (int k = c0 + tid; k < c1; k += blockDim.x) {
+    const int cell = k / o, i = k - cell * o;
     double t = 0.0;
     for (int j = 0; j < o; ++j) {
-      const long long node = (cell * p + j) % n_nodes;
-      t = fma(__dmul_rn(sc, phi[node]), diff[i * o + j], t);
+      const int node = (cell * p + j) % nn;
+      t = fma(__dmul_rn(sc, phi_s[node]), diff[i * o + j], t);
     }
+    e_s[k] = t;
     e[k] = t;
   }
-  __syncthreads();
-  // field diagnostics (k_field_diag) and level matrices for speeds = E (k_level_mats)
-  double m = 0.0, q = 0.0;
-  for (long long k = tid; k < n_dofs; k += blockDim.x) {
-    const double v = e[k];
-    m = fmax(m, fabs(v));
-    q = fma(pxw[k], v * v, q);
+  cluster.sync();
+  if (rank == 0) {
+    // field diagnostics (k_field_diag): max |E| and 0.5 w.E^2, 1024-slot trees
+    for (int k = tid; k < nd; k += blockDim.x) {
+      if (k >= c0 && k < c1) continue;
+      int owner = 0;
+      while (k >= share(nd, owner + 1)) ++owner;
+      e_s[k] = *cluster.map_shared_rank(&e_s[k], owner);
+    }
+    __syncthreads();
+    for (int t = tid; t < 1024; t += blockDim.x) {
+      const double v = t < nd ? e_s[t] : 0.0;
+      red[t] = t < nd ? fmax(0.0, fabs(v)) : 0.0;
+      red2[t] = t < nd ? fma(pxw[t], v * v, 0.0) : 0.0;
+    }
+    __syncthreads();
+    for (int st = 512; st > 0; st >>= 1) {
+      for (int t = tid; t < st; t += blockDim.x) {
+        red[t] = fmax(red[t], red[t + st]);
+        red2[t] += red2[t + st];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      diag2[0] = red[0];
+      diag2[1] = 0.5 * red2[0];
+    }
   }
-  red[tid] = m;
-  red2[tid] = q;
-  for (long long idx = tid; idx < n_dofs * n_levels; idx += blockDim.x) {
-    const int lev = (int)(idx / n_dofs);
-    const long long c = idx - (long long)lev * n_dofs;
+  // level matrices for speeds = E (k_level_mats): my columns, one thread per
+  // (level, column, A | B)
+  const int my = c1 - c0;
+  for (int idx = tid; idx < 2 * my * n_levels; idx += blockDim.x) {
+    const int ab = idx & 1, rest = idx >> 1;
+    const int lev = rest / my, c = c0 + (rest - lev * my);
     const double width = base_width / (double)(1LL << lev);
     long long ns;
     double a;
-    split_shift(e[c], dt, width, &ns, &a);
-    double A[O * O], B[O * O];
-    overlap_pair<O>(vb, a, A, B);
-    lm_ns[idx] = ns;
-    lm_frac[idx] = a;
+    split_shift(e_s[c], dt, width, &ns, &a);
+    if (ab == 0) {
+      lm_ns[(long long)lev * nd + c] = ns;
+      lm_frac[(long long)lev * nd + c] = a;
+    }
+    double M[O * O];
+    if (a == 0.0) {
 #pragma unroll
-    for (int k = 0; k < O * O; ++k) {
-      lm_mats[((long long)(lev * 2 + 0) * O * O + k) * n_dofs + c] = A[k];
-      lm_mats[((long long)(lev * 2 + 1) * O * O + k) * n_dofs + c] = B[k];
+      for (int k = 0; k < O * O; ++k) M[k] = (ab == 0 && k % (O + 1) == 0) ? 1.0 : 0.0;
+    } else {
+      double raw[O * O];
+      const double split = 2.0 * a - 1.0;
+      if (ab == 0)
+        interval_block<O>(vb, split, 1.0, -2.0 * a, raw);
+      else
+        interval_block<O>(vb, -1.0, split, 2.0 * (1.0 - a), raw);
+      apply_minv<O>(vb, raw, M);
     }
+#pragma unroll
+    for (int k = 0; k < O * O; ++k)
+      lm_mats[((long long)(lev * 2 + ab) * O * O + k) * nd + c] = M[k];
   }
-  __syncthreads();
-  for (int st = blockDim.x / 2; st > 0; st >>= 1) {
-    if (tid < st) {
-      red[tid] = fmax(red[tid], red[tid + st]);
-      red2[tid] += red2[tid + st];
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    diag2[0] = red[0];
-    diag2[1] = 0.5 * red2[0];
-  }
+  cluster.sync();   // no CTA leaves while another may still read its shared memory
 }
 
 }  // namespace sldg
@@ -1169,7 +1234,8 @@ int sldg_field_chain(const sldg_vplan* vp, const sldg_xplan* xp, const sldg_pois
                      double* phi, double* e, double* diag2, double* mom_prev3, void* scratch,
                      void* stream) {
   if (!vp || !xp || !P || !phi || !e || !diag2 || !scratch || !(dt > 0.0) ||
-      (!rho_in && !rho) || n_cols != P->n_dofs) {
+      (!rho_in && !rho) || n_cols != P->n_dofs || n_cols > kChainMaxDofs ||
+      P->n_nodes > kChainMaxDofs) {
     set_error("bad sldg_field_chain arguments");
     return SLDG_ERR_ARG;
   }
@@ -1191,7 +1257,8 @@ int sldg_field_chain(const sldg_vplan* vp, const sldg_xplan* xp, const sldg_pois
   switch (vp->o) {
 #define CASE(O)                                                                                \
   case O:                                                                                      \
-    SLDG_CUDA_TRY(launch_pdl(k_field_chain<O>, dim3(1), dim3(1024), 0, st, rho_in,           \
+    SLDG_CUDA_TRY(launch_pdl(k_field_chain<O>, dim3(kChainCtas), dim3(kChainThreads), 0, st,  \
+                             rho_in,                                                           \
                              (const double*)s.rho_part, (const double*)s.mom_part, grid,       \
                              mom_prev3, rho, (const double*)P->xw, (const double*)P->green,    \
                              (const double*)P->diff, P->n_cells, P->p, P->length, P->h,        \
