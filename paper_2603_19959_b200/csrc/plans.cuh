@@ -32,43 +32,6 @@ struct VPlanDev {
   double radius, base_width;
 };
 
-// Composed trailing + leading half x-steps of one unique speed (both use the row's
-// speed): C0 = A A, C1 = A B + B A, C2 = B B (OX*OX each) and the moment weights
-// cA = A^T xw, cB = B^T xw (OX each), every block padded to an even count so the fused
-// step reads them as 16-byte pairs.  A zero shift is (A, B) = (I, 0).
-template <int OX>
-struct XComp {
-  static constexpr int MP = (OX * OX + 1) & ~1, ZP = (OX + 1) & ~1;
-  static constexpr int CS = 3 * MP + 2 * ZP;    // doubles per speed (even)
-  static constexpr int CL = 3 * OX * OX + 2 * OX;   // logical entries per speed
-  // logical entry e of a speed with matrices A, B -> (padded position, value)
-  __device__ __forceinline__ static double entry(const double* A, const double* B,
-                                                 const double* xw, int e, int* pos) {
-    double v;
-    if (e < 3 * OX * OX) {
-      const int w = e / (OX * OX), k = (e / OX) % OX, j = e % OX;
-      *pos = w * MP + k * OX + j;
-      const double* L = w == 2 ? B : A;
-      const double* Rm = w == 0 ? A : B;
-      v = L[k * OX] * Rm[j];
-#pragma unroll
-      for (int m = 1; m < OX; ++m) v = fma(L[k * OX + m], Rm[m * OX + j], v);
-      if (w == 1) {
-#pragma unroll
-        for (int m = 0; m < OX; ++m) v = fma(B[k * OX + m], A[m * OX + j], v);
-      }
-    } else {
-      const int q = e - 3 * OX * OX, j = q % OX;
-      *pos = 3 * MP + (q < OX ? 0 : ZP) + j;
-      const double* M = q < OX ? A : B;
-      v = xw[0] * M[j];
-#pragma unroll
-      for (int k = 1; k < OX; ++k) v = fma(xw[k], M[k * OX + j], v);
-    }
-    return v;
-  }
-};
-
 }  // namespace sldg
 
 struct sldg_vplan {
@@ -88,7 +51,6 @@ struct XPlanDev {
   const double* mats;      // per unique speed: A (o*o) then B (o*o)
   const int* row_speed;    // per row
   const int* nsm;          // per unique speed: n_shift mod n_cells (periodic rows)
-  double* comp;            // per unique speed: composed X.X step (sldg_xplan_compose)
 };
 
 }  // namespace sldg
@@ -103,7 +65,6 @@ struct sldg_xplan {
                    // per-(cell, v_x node) speed (sldg_xplan_set_vlayout); 0 = unknown
   double h, dt;
   void* block;
-  const double* comp_xw;   // x weights the composed table was built with (nullptr: none)
 };
 
 struct sldg_poisson {
@@ -118,8 +79,6 @@ struct sldg_poisson {
 };
 
 namespace sldg {
-
-int xplan_compose(sldg_xplan* X, const double* xw, cudaStream_t st);
 
 template <int O>
 __device__ __forceinline__ void load_pair(const double* __restrict__ lm_mats, int lev,

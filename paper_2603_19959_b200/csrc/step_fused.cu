@@ -73,6 +73,7 @@ static __global__ void k_fold3(const double* __restrict__ part, long long n, dou
   if (lane == 0) out[w] = s;
 }
 
+constexpr int kFRing = 4;
 constexpr int kMaxLev = 8;
 
 struct FusedArgs {
@@ -90,6 +91,7 @@ using BoolC = std::integral_constant<bool, B>;
 // per-item tables in shared memory (two buffers: current item, next item)
 struct ItemTabs {
   long long* crow;   // [nmax] first row of each cell (line 0)
+  double* cm;        // [nmax][3][R] w, v0, v2 of the tile rows
   int* cg;           // [nmax][OV] x-speed index per (cell, v_x node)
 };
 
@@ -100,16 +102,12 @@ struct ItemTabs {
 //   1 last step of a run: V + X1 (+ moments), X1's result is the state (-> HBM);
 //   2 lead: the first half x-step alone, X1 (+ rho) -> HBM (no V) -- the tile
 //     distribution of the other modes, so a pencil-sharded rank touches only its rows.
-// RING: TMA ring slots (cell tiles in flight).  (Measured and rejected: three CTAs per
-// SM for the headline shape -- registers capped at 112 and a 3-slot ring: 0.69 ms against
-// 0.60 ms; with the tiles' b-sources carried in registers 0.85 ms.)
-template <int OV, int OX, int LG, int NXC, int MODE, int RING>
-__device__ __forceinline__ void
-step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout,
-                int n_cols_arg, int n_xc_arg, const double* __restrict__ speeds, int bc,
-                const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
-                int rw_arg, int n_speeds, int nmax, long long t_begin, long long n_tiles,
-                FusedArgs fa) {
+template <int OV, int OX, int LG, int NXC, int MODE>
+__global__ void __launch_bounds__(384, 1)
+k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout,
+             int n_cols_arg, int n_xc_arg, const double* __restrict__ speeds, int bc,
+             const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats, int rw_arg,
+             int n_speeds, int nmax, long long t_begin, long long n_tiles, FusedArgs fa) {
   const int n_xc = NXC > 0 ? NXC : n_xc_arg;
   const int n_cols = NXC > 0 ? OX * NXC : n_cols_arg;
   const int rw = NXC > 0 ? ((OX * NXC) | 1) : rw_arg;
@@ -118,31 +116,29 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
   // every block padded to an even count so the X phase reads them as 16-byte pairs
   constexpr int XMP = (OX * OX + 1) & ~1, XZP = (OX + 1) & ~1;
   constexpr int XCS = 3 * XMP + 2 * XZP;        // doubles per v_x node (even)
-  static_assert(XCS >= XM && XM % 2 == 0, "the side buffer also holds A | B per v_x node");
   constexpr int XCL = 3 * OX * OX + 2 * OX;     // logical entries per v_x node
   constexpr int R = LG * OV;                    // rows per tile
   constexpr int n_lg = OV * OV / LG;
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) unsigned long long full[RING];
+  __shared__ __align__(8) unsigned long long full[kFRing];
   __shared__ int s_nsmin[kMaxLev], s_nsmax[kMaxLev];
   __shared__ __align__(16) long long s_wd[2][2];   // walk descriptor per table buffer
 
   const int tile = R * n_cols;                  // doubles per ring slot
   double* ring = sm;
-  double* stA = ring + RING * tile;            // two tile buffers of R rows (stride rw)
-  int* xns = reinterpret_cast<int*>(stA + 2 * R * rw);   // per x-speed: integer shift
-  // per-tile side data, two buffers alternating like the tile buffers, filled by
-  // cp.async one tile ahead: the composed x-step of the tile's v_x nodes (MODE 0;
-  // C0 = A A, C1 = A B + B A, C2 = B B, cA = A^T xw, cB = B^T xw, from the x plan's
-  // table) and w, v0, v2 of the tile's rows
-  double* xcmp = stA + 2 * R * rw + 2 * ((n_speeds + 3) / 4);   // 16-byte aligned
-  double* scm = xcmp + 2 * OV * XCS;            // [2][3][R]
-  double* xw0 = scm + 2 * 3 * R;                // x quadrature weights of one cell
-  double* tabs0 = xw0 + ((OX + 1) & ~1);
-  const int tab_dbl = nmax + (nmax * OV + 1) / 2;
+  double* stA = ring + kFRing * tile;          // two tile buffers of R rows (stride rw)
+  double* xtab = stA + 2 * R * rw;                 // n_speeds x (A|B) for the x shift
+  int* xns = reinterpret_cast<int*>(xtab + (long long)n_speeds * XM);
+  // composed x-step per tile and v_x node (MODE 0), two buffers alternating like
+  // the tile buffers: C0 = A A, C1 = A B + B A, C2 = B B, then cA = A^T xw, cB = B^T xw
+  double* xcmp = xtab + (long long)n_speeds * XM + 2 * ((n_speeds + 3) / 4);   // 16-byte aligned
+  double* xw0 = xcmp + 2 * OV * XCS;            // x quadrature weights of one cell
+  double* tabs0 = xw0 + OX;
+  const int tab_dbl = nmax + 3 * R * nmax + (nmax * OV + 1) / 2;
   auto tabs = [&](int b) -> ItemTabs {
     double* base = tabs0 + (long long)b * tab_dbl;
-    return ItemTabs{reinterpret_cast<long long*>(base), reinterpret_cast<int*>(base + nmax)};
+    return ItemTabs{reinterpret_cast<long long*>(base), base + nmax,
+                    reinterpret_cast<int*>(base + nmax + 3 * R * nmax)};
   };
 
   const int tid = threadIdx.x;
@@ -160,8 +156,12 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
   const long long it_first = tb / nmax, it_last = (te - 1) / nmax;   // item range (inclusive)
   const int n_items = (int)(it_last - it_first + 1);
 
-  // x shifts; a zero shift is (A, B) = (I, 0) with no cell shift so the X phases run
-  // without a per-thread branch (1*u0 + 0*u1 + ... == u0)
+  // x-shift tables; a zero shift is stored as (A, B) = (I, 0) with no cell shift so
+  // the X phases run without a per-thread branch (1*u0 + 0*u1 + ... == u0)
+  for (int k = tid; k < n_speeds * XM; k += nthr) {
+    const int g = k / XM, e = k - g * XM;
+    xtab[k] = X.ident[g] ? ((e < OX * OX && e % (OX + 1) == 0) ? 1.0 : 0.0) : __ldg(X.mats + k);
+  }
   for (int k = tid; k < n_speeds; k += nthr) xns[k] = X.ident[k] ? 0 : (int)X.ns[k];
   if (tid < OX) xw0[tid] = __ldg(fa.xw + tid);   // uniform x grid: every cell's weights
   if (tid < kMaxLev) {
@@ -169,18 +169,17 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
     s_nsmax[tid] = -(1 << 30);
   }
   if (tid == 0) {
-    for (int k = 0; k < RING; ++k) mbar_init(&full[k], 1);
+    for (int k = 0; k < kFRing; ++k) mbar_init(&full[k], 1);
     mbar_fence_init();
   }
   __syncthreads();
 
   const bool per = (bc == SLDG_BC_PERIODIC);
-  // the headline instantiation launches exactly n_cols = OV * n_xc threads
-  const bool colv = (NXC > 0 && OX * NXC == OV * NXC) ? true : tid < n_cols;
+  const bool colv = tid < n_cols;
   const int c = tid;
 
   // ---- X-phase state: thread = (iv, x cell)
-  const bool xv = (NXC > 0 && OX == OV) ? true : tid < OV * n_xc;
+  const bool xv = tid < OV * n_xc;
   const int iv = xv ? tid / n_xc : 0;
   const int cx = xv ? tid - iv * n_xc : 0;
   // moments: each output row is contracted with the x weights first, then
@@ -217,6 +216,11 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
       const long long l0 = (long long)item_t0(it) * OV;
       for (int k = rt; k < n * OV; k += nthr)
         cp_async4(T.cg + k, X.row_speed + T.crow[k / OV] + l0 + k % OV);
+      for (int k = rt; k < n * 3 * R; k += nthr) {
+        const int s2 = k / (3 * R), rem = k - s2 * 3 * R, a = rem / R, r = rem - a * R;
+        const double* src = a == 0 ? fa.w : (a == 1 ? fa.v0 : fa.v2);
+        cp_async8(T.cm + k, src + T.crow[s2] + l0 + r);
+      }
     }
   };
   auto stage_sync = [&](int st, int b, long long it) {
@@ -227,32 +231,6 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
 
   // item 0 tables, synchronously
   for (int st = 0; st < 3; ++st) stage_sync(st, 0, it_first);
-  // side data of cell s's tile into buffer `par` by cp.async (warps 0-2; the pump is
-  // the last warp, the table stages start at the second-to-last): the composed x-step
-  // of its v_x nodes (MODE 0; the single step's A | B in modes 1 and 2) and w, v0, v2
-  // of its rows
-  auto side_copy = [&](int b, long long it, int s, int par) {
-    const ItemTabs T = tabs(b);
-    const long long l0 = (long long)item_t0(it) * OV;
-    constexpr int XS = MODE == 0 ? XCS : XM;     // doubles per v_x node (even)
-    constexpr int NCH = OV * XS / 2;             // 16-byte chunks
-    const double* tab = MODE == 0 ? X.comp : X.mats;
-    double* dc = xcmp + par * OV * XCS;
-    double* dm = scm + par * 3 * R;
-    const long long r0 = T.crow[s] + l0;
-    // matrices on the first warps, row weights from thread 64 on
-    for (int k = tid; k < NCH; k += nthr) {
-      const int jv = (2 * k) / XS, e = 2 * k - jv * XS;
-      cp_async16(dc + jv * XS + e, tab + (long long)T.cg[s * OV + jv] * XS + e);
-    }
-    for (int q = ((tid - 64) % nthr + nthr) % nthr; q < 3 * R; q += nthr) {
-      const int a = q / R, r = q - a * R;
-      const double* src = a == 0 ? fa.w : (a == 1 ? fa.v0 : fa.v2);
-      cp_async8(dm + q, src + r0 + r);
-    }
-  };
-  // the first tile's side data does not depend on E either
-  side_copy(0, it_first, item_sb(it_first), 0);
 
   // Everything above depends only on the plans and the state, so under
   // programmatic dependent launch it overlaps the preceding field chain; E and
@@ -310,9 +288,9 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
       }
       const int cell = ld_c < 0 ? n - 1 : (ld_c >= n ? 0 : ld_c);
       const long long row0 = tabs(b).crow[cell] + (long long)item_t0(it) * OV;
-      unsigned long long* bar = &full[issued % RING];
+      unsigned long long* bar = &full[issued & (kFRing - 1)];
       mbar_expect_tx(bar, (unsigned)(tile * 8));
-      bulk_g2s(ring + (issued % RING) * tile, fin + row0 * n_cols, (unsigned)(tile * 8), bar);
+      bulk_g2s(ring + (issued & (kFRing - 1)) * tile, fin + row0 * n_cols, (unsigned)(tile * 8), bar);
       ++issued;
       ++ld_c;
     }
@@ -396,7 +374,7 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
 
     // ===================== V: pencil sweep of cell s -> tile buffer (R rows, stride rw)
     auto v_pump = [&](int s) {
-      if (streamable && tid == pump_tid) pump(base + max(s - 1, first) - first + RING, i, n_staged >= 4);
+      if (streamable && tid == pump_tid) pump(base + max(s - 1, first) - first + kFRing, i, n_staged >= 4);
     };
     auto v_tile = [&](int s, double* dst) {
       if (streamable) {
@@ -404,11 +382,11 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
         // loads up to `waited` were waited for at earlier tiles (their slots are
         // not refilled before every thread is past them): only the new ones
         for (unsigned k = (unsigned)max(klo, waited + 1); k <= (unsigned)khi; ++k)
-          mbar_wait(&full[k % RING], (k / RING) & 1u);
+          mbar_wait(&full[k & (kFRing - 1)], (k / kFRing) & 1u);
         waited = max(waited, khi);
         if (colv) {
           double* out = dst + c;
-          auto slot = [&](int cell) { return ring + ((unsigned)(base + cell - first) % RING) * tile + c; };
+          auto slot = [&](int cell) { return ring + ((base + cell - first) & (kFRing - 1)) * tile + c; };
           if (speed == 0.0) {
             vcopy(out, slot(s));
           } else {
@@ -449,11 +427,18 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
     //     through the composed matrices; the moments take X1 at cell a (cx -> a is a
     //     bijection of the row's cells).
     //   MODE 1: X1 (+ moments) -> HBM;  MODE 2: X1 (+ rho) -> HBM.
-    auto x_tile = [&](int s, const double* src, const double* src_cmp, const double* src_cm) {
+    auto x_tile = [&](int s, const double* src, const double* src_cmp) {
       if (!xv) return;
-      const double* mcur = src_cm;
+      const double* mcur = T.cm + (long long)s * 3 * R;
       const long long r0 = T.crow[s] + l0;
       const int g = T.cg[s * OV + iv];
+      double xa[OX * OX], xb[OX * OX];
+      const double* AB = xtab + (long long)g * XM;
+#pragma unroll
+      for (int k = 0; k < OX * OX; ++k) {
+        xa[k] = AB[k];
+        xb[k] = AB[OX * OX + k];
+      }
       const int ns = xns[g];
       const int ca = wrap(cx - ns);
       double* dst = fout + (r0 + iv) * n_cols + cx * OX;
@@ -524,15 +509,6 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
           dst += (long long)OV * n_cols;
         }
       } else {
-        // the single half step's (A, B) of this v_x node, staged by x_side (a zero shift's
-        // pair is exactly (I, 0) in the plan, xfield.py:83-84)
-        double xa[OX * OX], xb[OX * OX];
-        const double* AB = src_cmp + iv * XM;
-#pragma unroll
-        for (int k = 0; k < OX * OX; ++k) {
-          xa[k] = AB[k];
-          xb[k] = AB[OX * OX + k];
-        }
         const int ia = ca * OX, ib = (ca == 0 ? n_xc - 1 : ca - 1) * OX;
 #pragma unroll
         for (int t = 0; t < LG; ++t) {
@@ -564,11 +540,42 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
         }
       }
     };
-    auto x_side = [&](int s2, int par) { side_copy(b, it, s2, par); };
+    // MODE 0: composed x-step of cell s's v_x nodes -> dst (XCS entries per node)
+    auto x_compose = [&](int s, double* dst) {
+      if (MODE != 0) return;
+      for (int e0 = tid; e0 < OV * XCL; e0 += nthr) {   // the CTA may have < OV*XCL threads
+        const int jv = e0 / XCL, e = e0 - jv * XCL;
+        int pos;   // padded position of logical entry e
+        const double* A = xtab + (long long)T.cg[s * OV + jv] * XM;
+        const double* B = A + OX * OX;
+        double v;
+        if (e < 3 * OX * OX) {
+          const int w = e / (OX * OX), k = (e / OX) % OX, j = e % OX;
+          pos = w * XMP + k * OX + j;
+          const double* L = w == 2 ? B : A;
+          const double* Rm = w == 0 ? A : B;
+          v = L[k * OX] * Rm[j];
+#pragma unroll
+          for (int m = 1; m < OX; ++m) v = fma(L[k * OX + m], Rm[m * OX + j], v);
+          if (w == 1) {
+#pragma unroll
+            for (int m = 0; m < OX; ++m) v = fma(B[k * OX + m], A[m * OX + j], v);
+          }
+        } else {
+          const int q = e - 3 * OX * OX, j = q % OX;
+          pos = 3 * XMP + (q < OX ? 0 : XZP) + j;
+          const double* M = q < OX ? A : B;
+          v = xw0[0] * M[j];
+#pragma unroll
+          for (int k = 1; k < OX; ++k) v = fma(xw0[k], M[k * OX + j], v);
+        }
+        dst[jv * XCS + pos] = v;
+      }
+    };
     // one CTA barrier per tile; the next item's table prefetch advances one stage
     // per barrier (copies issued after barrier k complete before barrier k + 1)
     auto tile_barrier = [&]() {
-      cp_async_wait_all();   // this tile's side data and table stage (issued one tile ago)
+      if (n_staged > 0 && n_staged <= 3) cp_async_wait_all();
       __syncthreads();
       if (has_next && n_staged < 3) stage(n_staged, b ^ 1, it + 1);
       ++n_staged;
@@ -579,7 +586,7 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
     // before the previous barrier; V(s+1) writes the buffer X(s-1) read before it;
     // the ring slot a pump refills was last read by a V before the previous barrier)
     v_pump(sb);
-    if (i > 0) x_side(sb, 0);   // (item 0's was issued before grid_dep_wait)
+    x_compose(sb, xcmp);
     v_tile(sb, stA);
     tile_barrier();
     for (int s = sb; s < se; ++s) {
@@ -587,9 +594,9 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
       double* cur = stA + (j & 1) * R * rw;
       double* nxt = stA + ((j + 1) & 1) * R * rw;
       if (s + 1 < se) v_pump(s + 1);
-      x_tile(s, cur, xcmp + (j & 1) * OV * XCS, scm + (j & 1) * 3 * R);
+      x_tile(s, cur, xcmp + (j & 1) * OV * XCS);
       if (s + 1 < se) {
-        x_side(s + 1, (j + 1) & 1);
+        x_compose(s + 1, xcmp + ((j + 1) & 1) * OV * XCS);
         v_tile(s + 1, nxt);
       }
       tile_barrier();
@@ -597,7 +604,7 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
     if (streamable && se > sb) base += last - first + 1;
     if (has_next && n_staged < 4) {
       // finish the next item's prefetch when this segment was too short to hide it
-      cp_async_wait_all();
+      if (n_staged >= 1) cp_async_wait_all();
       __syncthreads();
       for (int st = n_staged; st < 3; ++st) stage_sync(st, b ^ 1, it + 1);
     }
@@ -628,20 +635,6 @@ step_fused_body(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* 
     for (int k = 0; k < nthr; ++k) s += red[tid * nthr + k];
     fa.mom_part[blockIdx.x * 3 + tid] = s;
   }
-}
-
-#define SLDG_FUSED_PARAMS                                                                     \
-  VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout,           \
-      int n_cols_arg, int n_xc_arg, const double* __restrict__ speeds, int bc,                 \
-      const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats, int rw_arg,     \
-      int n_speeds, int nmax, long long t_begin, long long n_tiles, FusedArgs fa
-#define SLDG_FUSED_ARGS                                                                       \
-  P, X, fin, fout, n_cols_arg, n_xc_arg, speeds, bc, lm_ns, lm_mats, rw_arg, n_speeds, nmax,  \
-      t_begin, n_tiles, fa
-
-template <int OV, int OX, int LG, int NXC, int MODE>
-__global__ void __launch_bounds__(384, 1) k_step_fused(SLDG_FUSED_PARAMS) {
-  step_fused_body<OV, OX, LG, NXC, MODE, 4>(SLDG_FUSED_ARGS);
 }
 
 struct FusedGeom {
@@ -684,17 +677,17 @@ static FusedGeom fused_geom(const sldg_vplan* vp, const sldg_xplan* xp, long lon
   if (hl > xp->n_cells || hr > xp->n_cells) return no("fused step: shift wider than the row");
   g.rw = (int)n_cols + (n_cols % 2 == 0 ? 1 : 0);   // odd row stride: conflict-free columns
   g.nmax = vp->max_walk_cells;
-  const size_t fixed = sizeof(double) * (2 * ((xp->n_speeds + 3) / 4) +
-                                         2 * OV * (3 * ((OX * OX + 1) & ~1) + 2 * ((OX + 1) & ~1)) +
-                                         ((OX + 1) & ~1)) + 64;
+  const size_t fixed = sizeof(double) * (size_t)xp->n_speeds * 2 * OX * OX +
+                       sizeof(double) * (2 * ((xp->n_speeds + 3) / 4) +
+                                         2 * OV * (3 * ((OX * OX + 1) & ~1) + 2 * ((OX + 1) & ~1)) + OX) + 64;
   const size_t nmax = (size_t)g.nmax;
   const size_t budget = 227 * 1024 - 1024;
   g.lg = 0;
   for (int lg = 4; lg >= 1; --lg) {   // instantiated line groups: OV, 2 (even OV), 1
     if ((OV * OV) % lg || (lg != OV && lg != 2 && lg != 1)) continue;
     const size_t R = (size_t)lg * OV;
-    const size_t tables = 2 * sizeof(double) * (nmax + (nmax * OV + 1) / 2 + 3 * R);
-    const size_t smem = sizeof(double) * (4 * R * n_cols + 2 * R * g.rw) + fixed + tables;
+    const size_t tables = 2 * sizeof(double) * (nmax + 3 * R * nmax + (nmax * OV + 1) / 2);
+    const size_t smem = sizeof(double) * (kFRing * R * n_cols + 2 * R * g.rw) + fixed + tables;
     // the moment reduction stores 3 values per launched thread (blockDim rounded to 32)
     const size_t red = sizeof(double) * std::max<size_t>(OV * n_cols, 3 * ((threads + 31) / 32 * 32));
     if (smem <= budget && sizeof(double) * 2 * R * g.rw >= red) {
@@ -1069,8 +1062,6 @@ int launch_step(const sldg_vplan* vp, const sldg_xplan* xp, const FusedGeom& g, 
   }
   int rc = fused_grid(vp, xp, g, grid);
   if (rc) return rc;
-  // the composed X.X table the steady-state mode reads (built once per x weights)
-  if (mode == 0 && (rc = xplan_compose(const_cast<sldg_xplan*>(xp), fa.xw, st))) return rc;
   SLDG_CUDA_TRY(launch_pdl(k, dim3((unsigned)*grid), dim3(g.threads), g.smem, st, vp->dev,
                            xp->dev, fin, fout, (int)n_cols, (int)xp->n_cells, speeds, (int)bc,
                            (const long long*)s.lm_ns, (const double*)s.lm_mats, g.rw,

@@ -528,68 +528,6 @@ static bool xadv_vec(const sldg_xplan* X, const double* fin, const double* fout,
 
 using namespace sldg;
 
-namespace sldg {
-
-template <int OX>
-__global__ void k_xcompose(XPlanDev X, const double* __restrict__ xw, long long n_speeds) {
-  using XC = XComp<OX>;
-  __shared__ double w[OX];
-  if (threadIdx.x < OX) w[threadIdx.x] = xw[threadIdx.x];
-  __syncthreads();
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= n_speeds * XC::CL) return;
-  const long long g = idx / XC::CL;
-  const int e = (int)(idx - g * XC::CL);
-  double A[OX * OX], B[OX * OX];
-  const bool id = X.ident[g] != 0;
-#pragma unroll
-  for (int k = 0; k < OX * OX; ++k) {
-    A[k] = id ? ((k % (OX + 1) == 0) ? 1.0 : 0.0) : X.mats[g * 2 * OX * OX + k];
-    B[k] = id ? 0.0 : X.mats[g * 2 * OX * OX + OX * OX + k];
-  }
-  int pos = 0;
-  const double v = XC::entry(A, B, w, e, &pos);
-  X.comp[g * XC::CS + pos] = v;
-  if (e == 0) {   // padding entries stay defined (zero)
-    for (int q = OX * OX; q < XC::MP; ++q) {
-      X.comp[g * XC::CS + q] = 0.0;
-      X.comp[g * XC::CS + XC::MP + q] = 0.0;
-      X.comp[g * XC::CS + 2 * XC::MP + q] = 0.0;
-    }
-    for (int q = OX; q < XC::ZP; ++q) {
-      X.comp[g * XC::CS + 3 * XC::MP + q] = 0.0;
-      X.comp[g * XC::CS + 3 * XC::MP + XC::ZP + q] = 0.0;
-    }
-  }
-}
-
-// Build the plan's composed X.X table for the x weights `xw` (one cell's OX values, a
-// device pointer) on `st`, once per weights pointer (stream-ordered before the kernels
-// that read it).
-int xplan_compose(sldg_xplan* X, const double* xw, cudaStream_t st) {
-  if (X->comp_xw == xw || X->n_speeds == 0) return SLDG_OK;
-  const int threads = 128;
-  switch (X->o) {
-#define CASE(O)                                                                              \
-  case O: {                                                                                  \
-    const long long n = X->n_speeds * XComp<O>::CL;                                          \
-    k_xcompose<O><<<(unsigned)((n + threads - 1) / threads), threads, 0, st>>>(X->dev, xw,   \
-                                                                              X->n_speeds); \
-    break;                                                                                   \
-  }
-    CASE(2) CASE(3) CASE(4)
-#undef CASE
-    default:
-      set_error("composed x step: degree 1..3");
-      return SLDG_ERR_UNSUPPORTED;
-  }
-  SLDG_LAUNCH_CHECK("k_xcompose");
-  X->comp_xw = xw;
-  return SLDG_OK;
-}
-
-}  // namespace sldg
-
 extern "C" {
 
 int sldg_xplan_create(const SldgXPlanDesc* d, sldg_xplan** out) {
@@ -623,8 +561,6 @@ int sldg_xplan_create(const SldgXPlanDesc* d, sldg_xplan** out) {
   size_t o_rs = off; off = align_up(off + sizeof(int) * R, 256);
   size_t o_sp = off; off = align_up(off + sizeof(double) * S, 256);
   size_t o_nsm = off; off = align_up(off + sizeof(int) * S, 256);
-  const int cs = 3 * ((o * o + 1) & ~1) + 2 * ((o + 1) & ~1);   // XComp<o>::CS
-  size_t o_cmp = off; off = align_up(off + sizeof(double) * cs * S, 256);
   sldg_xplan* X = new sldg_xplan();
   cudaError_t ce = cudaMalloc(&X->block, off);
   if (ce != cudaSuccess) {
@@ -637,8 +573,6 @@ int sldg_xplan_create(const SldgXPlanDesc* d, sldg_xplan** out) {
   X->dev.mats = (double*)(base + o_m);
   X->dev.row_speed = (int*)(base + o_rs);
   X->dev.nsm = (int*)(base + o_nsm);
-  X->dev.comp = (double*)(base + o_cmp);
-  X->comp_xw = nullptr;
   double* dsp = (double*)(base + o_sp);
   if (d->n_rows > 0) {
     ce = cudaMemcpy((void*)X->dev.row_speed, d->row_speed, sizeof(int) * d->n_rows,
