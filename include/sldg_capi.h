@@ -182,10 +182,45 @@ int sldg_advect_x_slab(const sldg_xplan* plan, const double* f_in, int64_t ld_in
 int sldg_advect_x_slab_tiles_scratch(const sldg_xplan* plan, int64_t n_local, int64_t ld_in,
                                      size_t* bytes);
 int sldg_advect_x_slab_tiles(const sldg_xplan* plan, const double* row_base, int64_t ld_in,
-                             int64_t src_off, int64_t halo_l, int64_t n_local, double* f_out,
-                             int64_t ld_out, int64_t out_off, const double* w, const double* v0,
-                             const double* v2, const double* xw_local, double* mom_out3,
-                             double* rho_out, void* scratch, void* stream);
+                             int64_t src_off, int64_t halo_l, int64_t halo_r, int64_t n_local,
+                             double* f_out, int64_t ld_out, int64_t out_off, int32_t n_apply,
+                             int64_t row_begin, int64_t row_count, int32_t accumulate,
+                             const double* w, const double* v0, const double* v2,
+                             const double* xw_local, double* mom_out3, double* rho_out,
+                             void* scratch, void* stream);
+/*   n_apply 2: trailing + leading half steps in one pass (halo_l, halo_r at least twice
+ *   the plan's reach; the intermediate's moments over the local cells).  Rows
+ *   [row_begin, row_begin + row_count) (whole velocity cells) only; accumulate != 0 adds
+ *   this range's rho and moments onto rho_out / mom_out3 (row chunks of one pass, summed
+ *   in call order on one stream). */
+
+/* ---- x-slab halo exchange (upwind-only, per row) --------------------------------
+ * A row with x shift n >= 0 reads n_apply*(n+1) cells left of its slab, a row with n < 0
+ * n_apply*|n| cells right of it (identity rows none).  sldg_halo_pack gathers, for rows
+ * [row_begin, row_end), the cells the right neighbour needs (this slab's last cells of
+ * the left-reaching rows) into to_right and the cells the left neighbour needs into
+ * to_left; sldg_halo_unpack writes the neighbours' data into this slab's margins.  Every
+ * rank has the same rows and speeds, so the packed layouts match across ranks.
+ * Buffers: [left margin lw | n_local*o local | right margin] per row, stride ld. */
+typedef struct sldg_halo sldg_halo;
+int sldg_halo_create(const sldg_xplan* plan, int64_t n_local, int32_t n_apply, sldg_halo** out);
+int sldg_halo_destroy(sldg_halo* h);
+/* out4 = {offset, count} of the to_right / from_left data, then of to_left / from_right,
+ * in doubles, for rows [row_begin, row_end). */
+int sldg_halo_extent(const sldg_halo* h, int64_t row_begin, int64_t row_end, int64_t* out4);
+/* out2 = widest left / right halo in cells */
+int sldg_halo_reach(const sldg_halo* h, int64_t* out2);
+int sldg_halo_pack(const sldg_halo* h, const double* buf, int64_t ld, int64_t lw,
+                   int64_t row_begin, int64_t row_end, double* to_right, double* to_left,
+                   void* stream);
+int sldg_halo_unpack(const sldg_halo* h, double* buf, int64_t ld, int64_t lw,
+                     int64_t row_begin, int64_t row_end, const double* from_left,
+                     const double* from_right, void* stream);
+/* out[i] = parts[0][i] + parts[1][i] + ... in part (rank) order; parts is n_parts x n. */
+int sldg_sum_parts(const double* parts, int64_t n_parts, int64_t n, double* out, void* stream);
+/* out[i] = src[idx[i]] (compacts an all-gathered, padded rank-major buffer). */
+int sldg_gather_index(const double* src, const int64_t* idx, int64_t n, double* out,
+                      void* stream);
 
 /* rho[c] = sum_r w[r] f[r, c]  (deterministic two-stage column reduction).
  * scratch: sldg_rho_scratch_bytes(). */

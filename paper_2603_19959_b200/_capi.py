@@ -129,10 +129,22 @@ _SIGS = {
     "sldg_advect_x_slab_tiles_scratch": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64,
                                                    C.POINTER(C.c_size_t)]),
     "sldg_advect_x_slab_tiles": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
-                                           C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
-                                           C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                           C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                           C.c_int64, C.c_int64, C.c_int32, C.c_int64,
+                                           C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                                           C.c_void_p]),
+                                           C.c_void_p, C.c_void_p]),
+    "sldg_halo_create": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_void_p)]),
+    "sldg_halo_destroy": (C.c_int, [C.c_void_p]),
+    "sldg_halo_extent": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, c_int64_p]),
+    "sldg_halo_reach": (C.c_int, [C.c_void_p, c_int64_p]),
+    "sldg_halo_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                 C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sldg_halo_unpack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                   C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "sldg_sum_parts": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]),
+    "sldg_gather_index": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                    C.c_void_p]),
     "sldg_rho_scratch_bytes": (C.c_int, [C.c_int64, C.c_int64, C.POINTER(C.c_size_t)]),
     "sldg_rho": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
                            C.c_void_p, C.c_void_p]),

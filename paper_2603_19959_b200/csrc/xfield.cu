@@ -175,6 +175,30 @@ k_moments_partial(const double* __restrict__ f, long long ld, long long n_rows, 
 }
 
 // stage 2 of the moments: warp w sums component w (launch with 96 threads)
+// the same sums added onto `out` when acc != 0 (row chunks of one pass, in chunk order)
+__global__ void k_colsum_acc(const double* __restrict__ partial, long long n_chunks,
+                             long long n_cols, double* __restrict__ out, int acc) {
+  const int lane = threadIdx.x & 31;
+  const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (c >= n_cols) return;
+  double s = 0.0;
+  for (long long k = lane; k < n_chunks; k += 32) s += partial[k * n_cols + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[c] = acc ? out[c] + s : s;
+}
+
+__global__ void k_sum3_acc(const double* __restrict__ partial, long long n,
+                           double* __restrict__ out, int acc) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (w >= 3) return;
+  double s = 0.0;
+  for (long long k = lane; k < n; k += 32) s += partial[k * 3 + w];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) out[w] = acc ? out[w] + s : s;
+}
+
 __global__ void k_sum3(const double* __restrict__ partial, long long n, double* __restrict__ out) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (w >= 3) return;
@@ -440,14 +464,16 @@ namespace sldg {
 // Geometry of k_xx_tiles: depends only on the problem shape (bitwise-stable sums).
 // n_out: output cells per row (default: the periodic row); src_len: doubles staged
 // per source row (default: the row itself; an x slab stages its margins too)
-static XTGeom xt_geom(const sldg_xplan* X, long long n_out = -1, long long src_len = -1) {
+static XTGeom xt_geom(const sldg_xplan* X, long long n_out = -1, long long src_len = -1,
+                      long long n_rows = -1) {
   XTGeom g{};
   g.ok = false;
   const int ov = X->vo, ox = X->o;
   const long long nxc = n_out < 0 ? X->n_cells : n_out;
-  if (ov < 2 || ov > 4 || ox < 2 || ox > 4 || nxc > 512 || X->n_rows == 0) return g;
+  const long long rows = n_rows < 0 ? X->n_rows : n_rows;
+  if (ov < 2 || ov > 4 || ox < 2 || ox > 4 || nxc > 512 || rows == 0) return g;
   const int nl = ov * ov, nloc = nl * ov;
-  if (X->n_rows % nloc != 0) return g;
+  if (rows % nloc != 0) return g;
   g.tpc = (int)std::max<long long>(1, std::min<long long>(kXTMaxTpc, 512 / nxc));
   g.threads = (int)((g.tpc * nxc + 31) / 32 * 32);
   if (g.threads < 64) g.threads = 64;
@@ -471,7 +497,7 @@ static XTGeom xt_geom(const sldg_xplan* X, long long n_out = -1, long long src_l
     if (g.ok) break;
   }
   if (!g.ok) return g;
-  g.n_tiles = (X->n_rows / nloc) * (nl / g.rpt) * ov;
+  g.n_tiles = (rows / nloc) * (nl / g.rpt) * ov;
   if (g.n_tiles * g.tpc >= (1LL << 31)) {   // the kernel indexes tiles in 32 bits
     g.ok = false;
     return g;
@@ -493,7 +519,8 @@ static int launch_xt_t(const sldg_xplan* X, const XTGeom& g, const double* fin, 
     if (g.rpt == 3) k = k_xx_tiles<OV, OX, 3>;
   }
   SLDG_CUDA_TRY(smem_limit((const void*)k, (int)g.smem));
-  k<<<(unsigned)g.grid_, g.threads, g.smem, st>>>(X->dev, fin, fout, ld, X->n_rows, g.n_out,
+  const long long rows = g.n_tiles / ((OV * OV / g.rpt) * OV) * (OV * OV * OV);
+  k<<<(unsigned)g.grid_, g.threads, g.smem, st>>>(X->dev, fin, fout, ld, rows, g.n_out,
                                                   g.rpt, g.tpc, g.nring, (int)X->n_speeds, epi,
                                                   napply, mom ? 1 : 0, rho ? 1 : 0, rm);
   SLDG_LAUNCH_CHECK("k_xx_tiles");
@@ -504,7 +531,7 @@ static int launch_xt(const sldg_xplan* X, const XTGeom& g, const double* fin, do
                      long long ld, int napply, bool mom, bool rho, const XEpi& epi,
                      cudaStream_t st, const XRowMap* rmap = nullptr) {
   // default: periodic rows, output in place of the input layout
-  const XRowMap rm = rmap ? *rmap : XRowMap{g.src_len, 0, 0, 1, 0, ld};
+  const XRowMap rm = rmap ? *rmap : XRowMap{g.src_len, 0, 0, 1, 0, ld, 0};
   switch (X->vo * 10 + X->o) {
 #define CASE(A, B) \
   case A * 10 + B: return launch_xt_t<A, B>(X, g, fin, fout, ld, napply, mom, rho, epi, st, rm);
@@ -812,26 +839,40 @@ int sldg_advect_x_slab_tiles_scratch(const sldg_xplan* X, int64_t n_local, int64
     set_error("slab tile kernel: unsupported shape");
     return SLDG_ERR_UNSUPPORTED;
   }
+  // the whole-plan launch has the largest grid of any row range
   *bytes = sizeof(double) * (size_t)tg.grid_ * (3 + n_local * X->o) + 256;
   return SLDG_OK;
 }
 
 int sldg_advect_x_slab_tiles(const sldg_xplan* X, const double* row_base, int64_t ld_in,
-                             int64_t src_off, int64_t halo_l, int64_t n_local, double* fout,
-                             int64_t ld_out, int64_t out_off, const double* w, const double* v0,
-                             const double* v2, const double* xw_local, double* mom_out3,
-                             double* rho_out, void* scratch, void* stream) {
+                             int64_t src_off, int64_t halo_l, int64_t halo_r, int64_t n_local,
+                             double* fout, int64_t ld_out, int64_t out_off, int32_t n_apply,
+                             int64_t row_begin, int64_t row_count, int32_t accumulate,
+                             const double* w, const double* v0, const double* v2,
+                             const double* xw_local, double* mom_out3, double* rho_out,
+                             void* scratch, void* stream) {
   const bool mom = mom_out3 != nullptr, rho = rho_out != nullptr;
-  if (!X || !row_base || !fout || n_local < 1 || halo_l < X->halo_l || src_off < 0 ||
-      src_off + (halo_l + n_local + X->halo_r) * X->o > ld_in || out_off < 0 ||
-      out_off + n_local * X->o > ld_out || (mom && (!w || !v0 || !v2 || !xw_local)) ||
-      (rho && !w) || ((mom || rho) && !scratch)) {
-    set_error("bad advect_x_slab_tiles arguments (halo too narrow?)");
+  if (!X) {
+    set_error("null x plan");
     return SLDG_ERR_ARG;
   }
-  if (X->n_rows == 0) return SLDG_OK;
+  const long long nloc = (long long)X->vo * X->vo * X->vo;
+  // reach of the shifts: one application needs (halo_l, halo_r) >= the plan's, two need
+  // twice that, and at least (2, 1) cells for the intermediate's halo cells
+  const long long need_l = n_apply == 2 ? std::max<long long>(2, 2 * X->halo_l) : X->halo_l;
+  const long long need_r = n_apply == 2 ? std::max<long long>(1, 2 * X->halo_r) : X->halo_r;
+  if (!row_base || !fout || n_local < 1 || (n_apply != 1 && n_apply != 2) ||
+      halo_l < need_l || halo_r < need_r || halo_l > n_local || halo_r > n_local ||
+      src_off < 0 || src_off + (halo_l + n_local + halo_r) * X->o > ld_in || out_off < 0 ||
+      out_off + n_local * X->o > ld_out || (mom && (!w || !v0 || !v2 || !xw_local)) ||
+      (rho && !w) || ((mom || rho) && !scratch) || nloc == 0 || row_begin < 0 ||
+      row_count < 0 || row_begin % nloc || row_count % nloc || row_begin + row_count > X->n_rows) {
+    set_error("bad advect_x_slab_tiles arguments (halo too narrow? rows not whole cells?)");
+    return SLDG_ERR_ARG;
+  }
+  if (row_count == 0) return SLDG_OK;
   // whole padded rows are staged (16-byte aligned bulk copies)
-  const XTGeom tg = xt_geom(X, n_local, ld_in);
+  const XTGeom tg = xt_geom(X, n_local, ld_in, row_count);
   if (!tg.ok || (ld_in & 1) || (((unsigned long long)row_base) & 15)) {
     set_error("slab tile kernel: unsupported shape (rows too long / unaligned)");
     return SLDG_ERR_UNSUPPORTED;
@@ -842,17 +883,17 @@ int sldg_advect_x_slab_tiles(const sldg_xplan* X, const double* row_base, int64_
     epi.mom_part = (double*)scratch;
     epi.rho_part = (double*)scratch + 3 * (size_t)tg.grid_;
   }
-  const XRowMap rm{(int)ld_in, (int)src_off, (int)halo_l, 0, (int)out_off, ld_out};
-  int rc = launch_xt(X, tg, row_base, fout, ld_in, 1, mom, rho, epi, st, &rm);
+  const XRowMap rm{(int)ld_in, (int)src_off, (int)halo_l, 0, (int)out_off, ld_out, row_begin};
+  int rc = launch_xt(X, tg, row_base, fout, ld_in, n_apply, mom, rho, epi, st, &rm);
   if (rc) return rc;
   if (mom) {
-    k_sum3<<<1, 96, 0, st>>>(epi.mom_part, tg.grid_, mom_out3);
+    k_sum3_acc<<<1, 96, 0, st>>>(epi.mom_part, tg.grid_, mom_out3, accumulate);
     SLDG_LAUNCH_CHECK("k_sum3");
   }
   if (rho) {
     const long long row_len = n_local * X->o;
-    k_colsum<<<(unsigned)((row_len * 32 + 255) / 256), 256, 0, st>>>(epi.rho_part, tg.grid_,
-                                                                row_len, rho_out);
+    k_colsum_acc<<<(unsigned)((row_len * 32 + 255) / 256), 256, 0, st>>>(
+        epi.rho_part, tg.grid_, row_len, rho_out, accumulate);
     SLDG_LAUNCH_CHECK("k_colsum");
   }
   return SLDG_OK;

@@ -36,11 +36,12 @@ constexpr int kXTMaxTpc = 8;
 // cells of the row, sources wrap around.  x slabs (wrap = 0, the sharded state):
 // the input row is [left margin | local | right margin], src_len doubles copied
 // from the row start, halo-relative cell j at src_off + j*o, the local cells are
-// j = hl .. hl+n_xc-1 (no wrap: the halo covers every shift); outputs go to
-// out_off + cx*o of rows with stride ld_out.
+// j = hl .. hl+n_xc-1 (no wrap: the halo covers every shift, twice the reach for
+// NAPPLY == 2); outputs go to out_off + cx*o of rows with stride ld_out.  row_off: the
+// absolute first row of the launch (a chunk of whole velocity cells).
 struct XRowMap {
   int src_len, src_off, hl, wrap, out_off;
-  long long ld_out;
+  long long ld_out, row_off;
 };
 
 // RPT > 0: rows per tile fixed at compile time (row loops unrolled, tile -> row
@@ -86,7 +87,7 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     const int cell = tile / per_cell;
     const int rem = tile - cell * per_cell;
     const int iv = rem % OV, tg = rem / OV;
-    return (long long)cell * NLOC + tg * rpt * OV + iv;
+    return rm.row_off + (long long)cell * NLOC + tg * rpt * OV + iv;
   };
 
   // a slot is full when warp 0's bulk copies have landed and (epilogues) warp 1's
@@ -192,15 +193,41 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     };
     const double* src = ring + (long long)s * slot_dbl + tt * rpt * src_len;
     const double* mt = meta + ((long long)s * tpc + tt) * rpt * 3;
-    double* md = mid + tt * rpt * src_len;   // (X.X: periodic rows only, src_len == row_len)
+    double* md = mid + tt * rpt * src_len;   // intermediate rows, the source rows' layout
     if (napply == 2) {
       if (live) {
+        // slabs: the second application reads the intermediate on up to |n| + 1 cells
+        // beyond the local ones (left of them for n >= 0, right for n < 0); thread cx
+        // forms local cell cx (moments as on periodic rows) and, for cx < extra, one of
+        // those halo cells (sources within the doubled halo)
+        const int nsh = rm.wrap ? 0 : xnsm[g];
+        const int extra = rm.wrap ? 0 : (nsh >= 0 ? nsh + 1 : -nsh);
+        const int xcell = nsh >= 0 ? rm.hl - 1 - cx : rm.hl + n_xc + cx;   // halo-relative
+        const int xa_ = rm.src_off + (xcell - nsh) * OX;
 #pragma unroll(RPT > 0 ? RPT : 1)
         for (int u = 0; u < rpt; ++u) {
           double y[OX];
           xapply(src + u * src_len, y);
+          const int mo = rm.wrap ? cx * OX : rm.src_off + (rm.hl + cx) * OX;
 #pragma unroll
-          for (int k = 0; k < OX; ++k) md[u * src_len + cx * OX + k] = y[k];
+          for (int k = 0; k < OX; ++k) md[u * src_len + mo + k] = y[k];
+          if (cx < extra) {
+            const double* srow = src + u * src_len;
+            double z[OX];
+#pragma unroll
+            for (int k = 0; k < OX; ++k) {
+              double sa = xa[k * OX] * srow[xa_];
+              double sb = xb[k * OX] * srow[xa_ - OX];
+#pragma unroll
+              for (int j = 1; j < OX; ++j) {
+                sa = fma(xa[k * OX + j], srow[xa_ + j], sa);
+                sb = fma(xb[k * OX + j], srow[xa_ - OX + j], sb);
+              }
+              z[k] = sa + sb;
+            }
+#pragma unroll
+            for (int k = 0; k < OX; ++k) md[u * src_len + rm.src_off + xcell * OX + k] = z[k];
+          }
           if (mom) {
             const double w = mt[u * 3], wv0 = w * mt[u * 3 + 1], wv2 = w * mt[u * 3 + 2];
 #pragma unroll

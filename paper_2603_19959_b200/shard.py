@@ -9,17 +9,17 @@ sweep plan are replicated.  Per Strang step the only data exchanged are:
   * the all-gather of rho's local segment (N_x^DOF doubles in total) -- the
     1D Poisson solve is tiny and runs redundantly on every rank;
   * the per-rank diagnostics partials (3 doubles), summed in rank order.
-The v-sweep is column-local.  Because the x kernels compute every output
-from the same operands in the same order whether the row is periodic or a
-slab with halos, and rho's row partition does not depend on the column
-count, f and E are bitwise identical for any number of ranks.
+The v-sweep is column-local.  The x kernels compute every output from the
+same operands in the same order whether the row is periodic or a slab with
+halos; the reductions (rho, moments) are deterministic for a given rank count
+(fixed chunk and rank order) and agree with the single-device run to round-off.
 
 The state carries its halo margins in place: each buffer is
   [ left margin | local cells | right margin ]
 per row (margins rounded up to an even number of doubles so the local part
-stays 16-byte aligned), so halos are written straight into the margins and
-the slab kernel reads one strided buffer.  The communication layer uses
-torch.distributed P2P (NCCL over NVLink on GPUs; gloo in the CPU tests).
+stays 16-byte aligned); halos are packed and unpacked by libsldg kernels
+(per row, upwind side only) and exchanged with torch.distributed P2P (NCCL over
+NVLink on GPUs; gloo for the CPU tests of the host logic).
 """
 from __future__ import annotations
 
@@ -72,115 +72,243 @@ def margin_dofs(cells: int, o: int) -> int:
     return m + (m & 1)
 
 
-class HaloExchanger:
-    """Fill the left/right margins of a slab buffer from the ring neighbours.
+class Collectives:
+    """The exchanges of a sharded step over torch.distributed (NCCL between the GPUs of a
+    box; gloo for CPU tensors in tests).  A sharded advance() is a generator that yields
+    requests at its exchange points; `run` services them:
 
-    buf: (n_rows, lw + n_local*o + rw) tensor, lw/rw = margin widths in doubles;
-    the last hl cells of the left margin and the first hr cells of the right
-    margin are written.  Works on any torch device / process group.
-    """
+      ("sum", vec)          vec <- sum over ranks in rank order (all-gather + ordered add,
+                            never an unordered all-reduce: every rank gets the same bits)
+      ("allgather", loc, out, idx)   out <- the ranks' `loc` segments in rank order
+      ("halo", bufs, after) P2P with the ring neighbours: bufs = (to_right, to_left,
+                            from_left, from_right); `after()` (the unpack) runs on the
+                            communication stream once the data is in; resumes with the
+                            CUDA event the compute stream must wait on (None on CPU)
 
-    def __init__(self, rank, world, hl, hr, o, n_local, group=None):
-        if hl > n_local or hr > n_local:
-            raise ValueError(f"halo ({hl}, {hr}) wider than the slab ({n_local} cells)")
-        self.rank, self.world = rank, world
-        self.hl, self.hr, self.o, self.n_local = hl, hr, o, n_local
-        self.lw, self.rw = margin_dofs(hl, o), margin_dofs(hr, o)
-        self.group = group
+    `lockstep(gens)` services the same requests for ranks run one after another on one
+    device (tests)."""
+
+    def __init__(self, rank, world, group=None):
+        self.rank, self.world, self.group = rank, world, group
+        self._comm = None
         self._bufs = {}
 
-    def _buf(self, name, like, cols):
-        key = (name, like.device, like.shape[0], cols)
-        b = self._bufs.get(key)
-        if b is None:
-            import torch
-            b = torch.empty((like.shape[0], cols), dtype=like.dtype, device=like.device)
-            self._bufs[key] = b
-        return b
-
-    def exchange(self, buf):
+    def _buf(self, key, n, like):
         import torch
+        b = self._bufs.get(key)
+        if b is None or b.numel() < n or b.device != like.device:
+            b = torch.empty(n, dtype=like.dtype, device=like.device)
+            self._bufs[key] = b
+        return b[:n]
+
+    def sum(self, vec):
         import torch.distributed as dist
-        o, hl, hr, lw, nl = self.o, self.hl, self.hr, self.lw, self.n_local
-        loc0 = lw                      # first local double
-        loc1 = lw + nl * o             # one past the last local double
-        # to the right neighbour: my last hl cells (its left halo)
-        # to the left neighbour: my first hr cells (its right halo)
-        send_r = buf[:, loc1 - hl * o:loc1] if hl else None
-        send_l = buf[:, loc0:loc0 + hr * o] if hr else None
-        left_dst = buf[:, lw - hl * o:lw] if hl else None
-        right_dst = buf[:, loc1:loc1 + hr * o] if hr else None
         if self.world == 1:
-            if hl:
-                left_dst.copy_(send_r)
-            if hr:
-                right_dst.copy_(send_l)
-            return buf
-        left = (self.rank - 1) % self.world
-        right = (self.rank + 1) % self.world
-        ops = []
-        if hl:
-            sr = self._buf("sr", buf, hl * o)
-            sr.copy_(send_r)
-            rl = self._buf("rl", buf, hl * o)
-            ops += [dist.P2POp(dist.isend, sr, right, self.group),
-                    dist.P2POp(dist.irecv, rl, left, self.group)]
-        if hr:
-            sl = self._buf("sl", buf, hr * o)
-            sl.copy_(send_l)
-            rr = self._buf("rr", buf, hr * o)
-            ops += [dist.P2POp(dist.isend, sl, left, self.group),
-                    dist.P2POp(dist.irecv, rr, right, self.group)]
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-        if hl:
-            left_dst.copy_(rl)
-        if hr:
-            right_dst.copy_(rr)
-        del torch
-        return buf
-
-
-def allgather_segments(local, counts, group=None):
-    """Concatenate per-rank 1-D segments (rank order) on every rank."""
-    import torch
-    import torch.distributed as dist
-    world = len(counts)
-    if world == 1:
-        return local
-    width = max(counts)
-    pad = torch.zeros(width, dtype=local.dtype, device=local.device)
-    pad[:local.numel()] = local
-    out = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(out, pad, group=group)
-    return torch.cat([out[r][:counts[r]] for r in range(world)])
-
-
-def sum_in_rank_order(vec, group=None):
-    """Deterministic cross-rank sum: all-gather the partials, add them in rank order."""
-    import torch.distributed as dist
-    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+            return vec
+        parts = self._buf("sum", self.world * vec.numel(), vec)
+        dist.all_gather_into_tensor(parts, vec.contiguous().view(-1), group=self.group)
+        ordered_sum(parts.view(self.world, -1), vec.view(-1))
         return vec
-    import torch
-    world = dist.get_world_size(group)
-    parts = [torch.empty_like(vec) for _ in range(world)]
-    dist.all_gather(parts, vec.contiguous(), group=group)
-    acc = parts[0].clone()
-    for p in parts[1:]:
-        acc += p
-    return acc
+
+    def allgather(self, loc, out, idx):
+        """`loc` is this rank's segment padded to idx.max_width doubles."""
+        import torch.distributed as dist
+        if self.world == 1:
+            gather_index(loc, idx.index, out)
+            return out
+        gat = self._buf("ag_out", self.world * idx.max_width, loc)
+        dist.all_gather_into_tensor(gat, loc, group=self.group)
+        gather_index(gat, idx.index, out)
+        return out
+
+    def halo(self, to_right, to_left, from_left, from_right):
+        """Send to_right to the right neighbour and to_left to the left one; receive
+        from_left from the left neighbour and from_right from the right one (periodic
+        ring).  World 1: the slab is its own neighbour."""
+        import torch.distributed as dist
+        if self.world == 1:
+            if to_right.numel():
+                from_left.copy_(to_right)
+            if to_left.numel():
+                from_right.copy_(to_left)
+            return
+        left, right = (self.rank - 1) % self.world, (self.rank + 1) % self.world
+        ops = []
+        if to_right.numel():
+            ops += [dist.P2POp(dist.isend, to_right, right, self.group),
+                    dist.P2POp(dist.irecv, from_left, left, self.group)]
+        if to_left.numel():
+            ops += [dist.P2POp(dist.isend, to_left, left, self.group),
+                    dist.P2POp(dist.irecv, from_right, right, self.group)]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def run(self, gen):
+        """Drive one rank's advance() generator; returns its value."""
+        import torch
+        cuda = torch.cuda.is_available()
+        try:
+            req = next(gen)
+            while True:
+                kind = req[0]
+                res = None
+                if kind == "sum":
+                    self.sum(req[1])
+                elif kind == "allgather":
+                    self.allgather(req[1], req[2], req[3])
+                elif kind == "halo":
+                    (to_r, to_l, fr_l, fr_r), after = req[1], req[2]
+                    if cuda and to_r.is_cuda:
+                        # the exchange and the unpack on the communication stream, after
+                        # the packs; the compute stream waits only where it needs margins
+                        if self._comm is None:
+                            self._comm = torch.cuda.Stream()
+                        packed = torch.cuda.Event()
+                        packed.record()
+                        with torch.cuda.stream(self._comm):
+                            self._comm.wait_event(packed)
+                            self.halo(to_r, to_l, fr_l, fr_r)
+                            after()
+                            res = torch.cuda.Event()
+                            res.record()
+                    else:
+                        self.halo(to_r, to_l, fr_l, fr_r)
+                        after()
+                else:
+                    raise ValueError(f"unknown exchange request {kind!r}")
+                req = gen.send(res)
+        except StopIteration as stop:
+            return stop.value
+
+    @staticmethod
+    def lockstep(gens):
+        """Drive the advance() generators of ranks 0..W-1 on one device in lockstep:
+        every rank runs to its next exchange point, then the exchange is done for all of
+        them (same arithmetic as `run` over NCCL).  Returns the ranks' values."""
+        import torch
+        world = len(gens)
+        out = [None] * world
+        reqs = []
+        for r, g in enumerate(gens):
+            try:
+                reqs.append(next(g))
+            except StopIteration as stop:
+                out[r] = stop.value
+                reqs.append(None)
+        while any(q is not None for q in reqs):
+            kinds = {q[0] for q in reqs if q is not None}
+            if len(kinds) != 1 or any(q is None for q in reqs):
+                raise RuntimeError(f"ranks out of step: {kinds}")
+            kind = kinds.pop()
+            if kind == "sum":
+                parts = torch.stack([q[1].reshape(-1) for q in reqs])
+                tot = torch.empty_like(parts[0])
+                ordered_sum(parts, tot)
+                for q in reqs:
+                    q[1].view(-1).copy_(tot)
+            elif kind == "allgather":
+                cat = torch.cat([q[1] for q in reqs])
+                for q in reqs:
+                    gather_index(cat, q[3].index, q[2])
+            elif kind == "halo":
+                for r, q in enumerate(reqs):
+                    fr_l, fr_r = q[1][2], q[1][3]
+                    left, right = reqs[(r - 1) % world], reqs[(r + 1) % world]
+                    if fr_l.numel():
+                        fr_l.copy_(left[1][0])
+                    if fr_r.numel():
+                        fr_r.copy_(right[1][1])
+                for q in reqs:
+                    q[2]()
+            else:
+                raise ValueError(f"unknown exchange request {kind!r}")
+            nxt = []
+            for r, g in enumerate(gens):
+                try:
+                    nxt.append(g.send(None))
+                except StopIteration as stop:
+                    out[r] = stop.value
+                    nxt.append(None)
+            reqs = nxt
+        return out
+
+
+def ordered_sum(parts, out):
+    """out[i] = parts[0][i] + parts[1][i] + ... in row order (libsldg, on the device)."""
+    from . import _capi
+    from ._device import current_stream
+    _capi.check(_capi.lib().sldg_sum_parts(parts.data_ptr(), parts.shape[0], parts.shape[1],
+                                           out.data_ptr(), current_stream()), ValueError)
+    return out
+
+
+def gather_index(src, idx, out):
+    from . import _capi
+    from ._device import current_stream
+    _capi.check(_capi.lib().sldg_gather_index(src.data_ptr(), idx.data_ptr(), out.numel(),
+                                              out.data_ptr(), current_stream()), ValueError)
+    return out
+
+
+class SegmentIndex:
+    """Positions of the ranks' segments in an all-gathered buffer padded to the widest."""
+
+    def __init__(self, counts, device):
+        import torch
+        self.max_width = max(counts)
+        pos = np.concatenate([r * self.max_width + np.arange(c) for r, c in enumerate(counts)])
+        self.index = torch.from_numpy(pos.astype(np.int64)).to(device)
+
+
+class HaloPlan:
+    """Per-row upwind halo layout of one x plan on a slab (libsldg sldg_halo)."""
+
+    def __init__(self, x_plan, n_local, n_apply):
+        import ctypes as C
+
+        from . import _capi
+        h = C.c_void_p()
+        _capi.check(_capi.lib().sldg_halo_create(x_plan.device_handle(), n_local, n_apply,
+                                                 C.byref(h)), ValueError)
+        self.h = h.value
+        r = np.zeros(2, dtype=np.int64)
+        _capi.check(_capi.lib().sldg_halo_reach(self.h, _capi.i64ptr(r)))
+        self.reach_l, self.reach_r = int(r[0]), int(r[1])
+        self.n_apply = n_apply
+
+    def extent(self, r0, r1):
+        from . import _capi
+        e = np.zeros(4, dtype=np.int64)
+        _capi.check(_capi.lib().sldg_halo_extent(self.h, r0, r1, _capi.i64ptr(e)))
+        return [int(v) for v in e]
+
+    def __del__(self):
+        try:
+            from . import _capi
+            _capi.lib().sldg_halo_destroy(self.h)
+        except Exception:
+            pass
 
 
 class ShardedSimulation:
-    """Strang step on an x-slab of the state, one rank per GPU.
+    """The Strang step on an x-slab of the state, one rank per GPU.
 
-    Same step as driver.Simulation: half-x (with halo exchange), rho of the
-    local columns all-gathered -> Poisson on every rank -> E, v-sweep of the
-    local columns, half-x (halo exchange), diagnostics (local partials summed
-    in rank order).  f lives in [margin | local | margin] buffers.
+    The velocity mesh and plans are replicated; the state is split along x into
+    contiguous slabs of cells, each row stored as [left margin | local | right margin].
+    advance() is pipelined like Simulation.advance(): the trailing half x-step of step k
+    and the leading one of step k + 1 run as ONE pass (k_xx_tiles, n_apply = 2) after one
+    exchange of doubled upwind halos, so a step is  V (column-local) -> halo exchange ->
+    X.X (+ moments of the intermediate, + rho of the result) -> all-gather of rho ->
+    Poisson (every rank, the whole x grid) -> E.  The exchange is per row and upwind only
+    (sldg_halo_pack/unpack: a row with shift n >= 0 needs 2n + 2 cells from the left, n < 0
+    2|n| from the right), split into row chunks: the chunks' NCCL send/recv and unpack run
+    on a communication stream while the compute stream runs the X.X of the chunks whose
+    margins are in (fewer exchanges, overlapped with the x update).
+    The reductions are deterministic for a given rank count (chunk order, rank order).
     """
 
-    def __init__(self, config, rank, world, group=None, mesh=None):
+    def __init__(self, config, rank, world, group=None, mesh=None, n_chunks=4):
         import torch
 
         from ._device import device, to_device_f64
@@ -194,7 +322,10 @@ class ShardedSimulation:
 
         self.config = config.validate()
         c = self.config
+        if c.dim != 3:
+            raise ValueError("x-slab sharding needs the 3V velocity layout")
         self.rank, self.world, self.group = rank, world, group
+        self.comm = Collectives(rank, world, group)
         self.basis = DGBasis(c.degree)
         self.mesh = mesh if mesh is not None else build_mesh(c.dim, c.n_base, c.levels, c.radius)
         self.perm = build_permutation(self.basis, c.dim)
@@ -209,14 +340,17 @@ class ShardedSimulation:
         self.cell0 = self.part.start(rank)
         o = self.xgrid.degree + 1
         self.o = o
-        hl, hr = x_halo_cells(self.xgrid.h, self.vcoords[:, 0], 0.5 * c.dt)
-        self.halo = HaloExchanger(rank, world, hl, hr, o, self.n_local, group)
-        self.lw, self.rw = self.halo.lw, self.halo.rw
-        self.width = self.lw + self.n_local * o + self.rw
-        # x plan over the full periodic grid (shifts and matrices are per speed)
         self.x_plan = precompute_x_matrices(self.xgrid, self.vcoords[:, 0], 0.5 * c.dt)
-        if c.dim == 3:
-            self.x_plan.velocity_order = c.degree + 1   # enables the row-tile slab kernel
+        self.x_plan.velocity_order = c.degree + 1   # the row-tile kernel's layout
+        self.halo1 = HaloPlan(self.x_plan, self.n_local, 1)
+        self.halo2 = HaloPlan(self.x_plan, self.n_local, 2)
+        # margins: the doubled reach (X.X), at least 2 cells left / 1 right (the X.X
+        # intermediate's halo cells), rounded to an even number of doubles
+        self.hl = max(2, self.halo2.reach_l)
+        self.hr = max(1, self.halo2.reach_r)
+        self.lw, self.rw = margin_dofs(self.hl, o), margin_dofs(self.hr, o)
+        width = self.lw + self.n_local * o + self.rw
+        self.width = width + (width & 1)
         self.poisson = PoissonSolver(self.xgrid)
         dev = device()
         self._vw = to_device_f64(self.vweights)
@@ -228,14 +362,36 @@ class ShardedSimulation:
         self._F = torch.zeros((n_v, self.width), dtype=torch.float64, device=dev)
         self._G = torch.zeros_like(self._F)
         sample_initial_into(c, self.vcoords, self.xgrid.dof_coords[x0:x1], self.f)
-        self._rho_loc = torch.empty(self.n_local * o, dtype=torch.float64, device=dev)
+        self._segs = SegmentIndex([n * o for n in self.part.counts()], dev)
+        # this slab's rho, padded to the widest slab (the all-gather's send buffer)
+        self._rho_loc = torch.zeros(self._segs.max_width, dtype=torch.float64, device=dev)
+        self._rho = torch.empty(self.xgrid.n_dofs, dtype=torch.float64, device=dev)
         self._phi = torch.empty(self.poisson.n_nodes, dtype=torch.float64, device=dev)
         self._e = torch.empty(self.xgrid.n_dofs, dtype=torch.float64, device=dev)
         self._rec = torch.empty(5, dtype=torch.float64, device=dev)
+        # row chunks (whole velocity cells) of the overlapped exchange
+        nloc = (c.degree + 1) ** 3
+        n_cells = n_v // nloc
+        k = max(1, min(int(n_chunks), n_cells))
+        bounds = [(i * n_cells // k) * nloc for i in range(k + 1)]
+        self.chunks = [(bounds[i], bounds[i + 1]) for i in range(k) if bounds[i + 1] > bounds[i]]
+        self._hbuf = {}
+        for hp in (self.halo1, self.halo2):
+            tot = hp.extent(0, n_v)
+            n_r, n_l = tot[1], tot[3]
+            self._hbuf[hp.n_apply] = [torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+                                      for n in (n_r, n_l, n_r, n_l)]
+        import ctypes as C
+
+        from . import _capi
+        nb = C.c_size_t()
+        _capi.check(_capi.lib().sldg_advect_x_slab_tiles_scratch(
+            self.x_plan.device_handle(), self.n_local, self.width, C.byref(nb)), ValueError)
+        self._xscratch = torch.empty(nb.value, dtype=torch.uint8, device=dev)
         self.t = 0.0
 
     def fused_step_supported(self) -> bool:
-        return False   # the one-pass step needs whole rows; slabs use the separate passes
+        return False   # the one-pass step needs whole rows; slabs run V and X.X passes
 
     # views ------------------------------------------------------------------
     def _local(self, buf):
@@ -246,119 +402,114 @@ class ShardedSimulation:
         """Local slab of the state (view into the margin buffer)."""
         return self._local(self._F)
 
-    @property
-    def _e_local(self):
-        x0 = self.cell0 * self.o
-        return self._e[x0:x0 + self.n_local * self.o]
+    def _swap(self):
+        self._F, self._G = self._G, self._F
 
-    # operators --------------------------------------------------------------
-    def _advect_x(self):
+    # building blocks --------------------------------------------------------
+    def _exchange(self, hp):
+        """Generator: pack every chunk, then one "halo" request per chunk; returns the
+        per-chunk events the X pass waits on."""
         from . import _capi
         from ._device import current_stream
-        self.halo.exchange(self._F)
-        hl, hr = self.halo.hl, self.halo.hr
-        o = self.o
-        src = self._F[:, self.lw - hl * o:]
-        _capi.check(_capi.lib().sldg_advect_x_slab(
-            self.x_plan.device_handle(), src.data_ptr(), self._F.stride(0), hl, hr,
-            self.n_local, self._G[:, self.lw:].data_ptr(), self._G.stride(0),
-            current_stream()), ValueError)
-        self._F, self._G = self._G, self._F
+        lib = _capi.lib()
+        to_r, to_l, fr_l, fr_r = self._hbuf[hp.n_apply]
+        ext = [hp.extent(r0, r1) for r0, r1 in self.chunks]
+        for (r0, r1), e in zip(self.chunks, ext):
+            _capi.check(lib.sldg_halo_pack(hp.h, self._F.data_ptr(), self.width, self.lw, r0, r1,
+                                           to_r[e[0]:].data_ptr(), to_l[e[2]:].data_ptr(),
+                                           current_stream()), ValueError)
+        events = []
+        for (r0, r1), e in zip(self.chunks, ext):
+            bufs = (to_r[e[0]:e[0] + e[1]], to_l[e[2]:e[2] + e[3]],
+                    fr_l[e[0]:e[0] + e[1]], fr_r[e[2]:e[2] + e[3]])
 
-    def _x_tiles(self, rho_out=None, mom_out3=None):
-        """Half x-step of the slab with the row-tile kernel, rho of the result (local
-        columns) or the moments of the result fused in; False if the kernel does not
-        cover this slab (then nothing was done)."""
-        import ctypes as C
+            def unpack(r0=r0, r1=r1, e=e):
+                _capi.check(lib.sldg_halo_unpack(hp.h, self._F.data_ptr(), self.width, self.lw,
+                                                 r0, r1, fr_l[e[0]:].data_ptr(),
+                                                 fr_r[e[2]:].data_ptr(), current_stream()),
+                            ValueError)
+            events.append((yield ("halo", bufs, unpack)))
+        return events
+
+    def _x_pass(self, n_apply, events, rho_out=None, mom_out3=None):
+        """X (n_apply 1) or X.X (2) of every chunk F -> G, each after its halo event."""
+        import torch
 
         from . import _capi
-        from ._device import SCRATCH, current_stream
-        if getattr(self, "_tiles_ok", None) is False:
-            return False
-        o, hl = self.o, self.halo.hl
+        from ._device import current_stream
         lib = _capi.lib()
-        if getattr(self, "_tiles_ok", None) is None:
-            nb = C.c_size_t()
-            self._tiles_ok = lib.sldg_advect_x_slab_tiles_scratch(
-                self.x_plan.device_handle(), self.n_local, self._F.stride(0), C.byref(nb)) == 0 \
-                and self._F.stride(0) % 2 == 0
-            self._tiles_bytes = nb.value
-            if not self._tiles_ok:
-                return False
-        self.halo.exchange(self._F)
-        scratch = SCRATCH.get(("xslab", id(self)), self._tiles_bytes)
-        _capi.check(lib.sldg_advect_x_slab_tiles(
-            self.x_plan.device_handle(), self._F.data_ptr(), self._F.stride(0),
-            self.lw - hl * o, hl, self.n_local, self._G.data_ptr(), self._G.stride(0), self.lw,
-            self._vw.data_ptr(), self._v0.data_ptr(), self._v2.data_ptr(), self._xw.data_ptr(),
-            None if mom_out3 is None else mom_out3.data_ptr(),
-            None if rho_out is None else rho_out.data_ptr(), scratch.data_ptr(),
-            current_stream()), ValueError)
-        self._F, self._G = self._G, self._F
-        return True
+        src_off = self.lw - self.hl * self.o
+        for i, (r0, r1) in enumerate(self.chunks):
+            if events[i] is not None:
+                torch.cuda.current_stream().wait_event(events[i])
+            _capi.check(lib.sldg_advect_x_slab_tiles(
+                self.x_plan.device_handle(), self._F.data_ptr(), self.width, src_off, self.hl,
+                self.hr, self.n_local, self._G.data_ptr(), self.width, self.lw, n_apply, r0,
+                r1 - r0, 1 if i else 0, self._vw.data_ptr(), self._v0.data_ptr(),
+                self._v2.data_ptr(), self._xw.data_ptr(),
+                None if mom_out3 is None else mom_out3.data_ptr(),
+                None if rho_out is None else rho_out.data_ptr(), self._xscratch.data_ptr(),
+                current_stream()), ValueError)
+        self._swap()
 
-    def _solve_from_local_rho(self, e_out):
-        rho = allgather_segments(self._rho_loc, [n * self.o for n in self.part.counts()],
-                                 self.group)
-        self.poisson.solve_into(rho.contiguous(), self._phi, e_out)
-
-    def _field(self, e_out):
-        from .xfield import rho_into
-        rho_into(self.f, self._vw, self._rho_loc)
-        self._solve_from_local_rho(e_out)
-
-    def _advect_v(self, e):
+    def _v_pass(self, e):
         from .vsweep import advect_velocity_into
         c = self.config
         x0 = self.cell0 * self.o
-        e_loc = e[x0:x0 + self.n_local * self.o]
-        advect_velocity_into(self.f, self._local(self._G), e_loc, c.dt, self.sweep_plan, c.bc,
-                             c.force_slow)
-        self._F, self._G = self._G, self._F
+        advect_velocity_into(self.f, self._local(self._G), e[x0:x0 + self.n_local * self.o],
+                             c.dt, self.sweep_plan, c.bc, c.force_slow)
+        self._swap()
 
-    def _diag_into(self, e, rec5):
-        from .driver import _moments_into
+    def _field(self, e_out, diag2):
         from .xfield import field_diag_into
-        field_diag_into(self.poisson, e, rec5[0:2])
-        _moments_into(self.f, self._vw, self._v0, self._v2, self._xw, rec5[2:5])
-        rec5[2:5] = sum_in_rank_order(rec5[2:5].clone(), self.group)
+        self.poisson.solve_into(self._rho, self._phi, e_out)
+        if diag2 is not None:
+            field_diag_into(self.poisson, e_out, diag2)
 
-    def enqueue_step(self, e_buf, rec5, v_event=None):
-        """One Strang step: 3 passes over the slab when the row-tile slab kernel covers
-        it (x + rho, v, x + moments), else x, rho, v, x, moments."""
+    # the pipelined Strang steps ------------------------------------------------
+    def advance_steps(self, n_steps, table, v_events=None):
+        """Generator form of advance() (exchange points yielded to a Collectives driver);
+        v_events[k] = (start, end) CUDA events recorded around step k's v-sweep."""
         import torch
-
-        from .xfield import field_diag_into
-        if self._x_tiles(rho_out=self._rho_loc):
-            self._solve_from_local_rho(e_buf)
-        else:
-            self._advect_x()
-            self._field(e_buf)
-        if v_event is not None:
-            v_event[0].record(torch.cuda.current_stream())
-        self._advect_v(e_buf)
-        if v_event is not None:
-            v_event[1].record(torch.cuda.current_stream())
-        if self._x_tiles(mom_out3=rec5[2:5]):
-            rec5[2:5] = sum_in_rank_order(rec5[2:5].clone(), self.group)
-            field_diag_into(self.poisson, e_buf, rec5[0:2])
-        else:
-            self._advect_x()
-            self._diag_into(e_buf, rec5)
+        if n_steps == 0:
+            return table
+        # leading half x-step of step 0 (+ rho of the slab), rho all-gathered
+        ev = yield from self._exchange(self.halo1)
+        self._x_pass(1, ev, rho_out=self._rho_loc)
+        yield ("allgather", self._rho_loc, self._rho, self._segs)
+        for k in range(n_steps):
+            self._field(self._e, table[k, 0:2])
+            if v_events is not None:
+                v_events[k][0].record(torch.cuda.current_stream())
+            self._v_pass(self._e)
+            if v_events is not None:
+                v_events[k][1].record(torch.cuda.current_stream())
+            last = k + 1 == n_steps
+            hp = self.halo1 if last else self.halo2
+            ev = yield from self._exchange(hp)
+            mom = table[k, 2:5]
+            if last:   # trailing half step (+ moments): the state of the step
+                self._x_pass(1, ev, mom_out3=mom)
+            else:      # trailing + next leading half steps (+ moments, + rho)
+                self._x_pass(2, ev, rho_out=self._rho_loc, mom_out3=mom)
+            yield ("sum", mom)
+            if not last:
+                yield ("allgather", self._rho_loc, self._rho, self._segs)
+        return table
 
     def advance(self, n_steps, table=None, v_events=None):
+        """n_steps Strang steps of the slab; row k of the returned (n_steps, 5) table is
+        step k's [max|E|, e_field, m0, m1, m2] (global, the same on every rank)."""
         import torch
         if table is None:
             table = torch.empty((n_steps, 5), dtype=torch.float64, device=self._F.device)
-        for k in range(n_steps):
-            self.enqueue_step(self._e, table[k], None if v_events is None else v_events[k])
-        return table
+        return self.comm.run(self.advance_steps(n_steps, table, v_events))
 
     def step(self):
         from .driver import DiagnosticsRecord
-        self.enqueue_step(self._e, self._rec)
+        table = self.advance(1)
         self.t += self.config.dt
-        r = self._rec.cpu().numpy()
+        r = table[0].cpu().numpy()
         return DiagnosticsRecord(self.t, float(r[0]), float(r[2]), float(r[3]), float(r[4]),
                                  float(r[1]), 0.5 * float(r[4]) + float(r[1]))
 
@@ -382,14 +533,15 @@ class PencilShardedSimulation(Simulation):
     advances only its contiguous share of whole items (rows of other ranks are never
     read or written here); the only exchange per step is the rank's partial sums
     [rho (N_x^DOF) | m0 m1 m2], added in rank order on every rank
-    (sum_in_rank_order) so all ranks solve the same Poisson problem.  Total work
+    (Collectives.sum) so all ranks solve the same Poisson problem.  Total work
     is fixed as ranks are added (strong scaling).
 
-    `reducer(vec) -> vec` replaces the cross-rank sum (tests run ranks in lockstep
-    on one device).
+    advance() is a generator at heart (advance_steps): its one exchange per step is a
+    ("sum", partials) request serviced by a Collectives driver (NCCL across processes,
+    or Collectives.lockstep for ranks run on one device in tests).
     """
 
-    def __init__(self, config, rank, world, group=None, mesh=None, reducer=None):
+    def __init__(self, config, rank, world, group=None, mesh=None):
         super().__init__(config, mesh=mesh)
         if not self.fused_step_supported():
             raise ValueError("pencil sharding needs a plan the fused step covers "
@@ -405,10 +557,11 @@ class PencilShardedSimulation(Simulation):
             (int(v) for v in info)
         self._tile_range = item_tile_range(self.n_tiles, self.cells_per_pencil, rank, world)
         self.rank, self.world, self.group = rank, world, group
-        self._reducer = reducer if reducer is not None else \
-            (lambda v: sum_in_rank_order(v, group))
-        self._part = torch.zeros(self._f.shape[1] + 3, dtype=torch.float64,
-                                 device=self._f.device)
+        self.comm = Collectives(rank, world, group)
+        n = self._f.shape[1]
+        self._part = torch.zeros(n + 3, dtype=torch.float64, device=self._f.device)
+        self._rho_idx = torch.arange(n, dtype=torch.int64, device=self._f.device)
+        self._mom_idx = torch.arange(n, n + 3, dtype=torch.int64, device=self._f.device)
 
     def owned_rows(self) -> np.ndarray:
         """Rows of f this rank advances: the rows of its tiles (tile t = cell
@@ -437,11 +590,49 @@ class PencilShardedSimulation(Simulation):
             scratch.data_ptr(), current_stream()), ValueError)
         return self._part
 
-    def _take_sums(self, tot, mom3=None):
+    def advance_steps(self, n_steps: int, table, v_events=None):
+        """Generator form of advance(): the rank's partial sums [rho | m0 m1 m2] are
+        yielded for the rank-order sum, which lands in place; v_events[k] = (start, end)
+        events around step k's fused kernel."""
+        import torch
+
+        from . import _capi
+        from ._device import current_stream
+        if n_steps == 0:
+            return table
+        e = self._e
         n = self._f.shape[1]
-        self._rho.copy_(tot[:n])
-        if mom3 is not None:
-            mom3.copy_(tot[n:])
+        lib = _capi.lib()
+
+        def take_rho():   # the summed rho of all ranks -> this rank's Poisson input
+            _capi.check(lib.sldg_gather_index(self._part.data_ptr(), self._rho_idx.data_ptr(),
+                                              n, self._rho.data_ptr(), current_stream()))
+
+        # leading half x-step of step 0 on my tiles, rho summed over the ranks
+        self._fused_step_deferred(e, mode=2)
+        self._fold_partials(False)
+        yield ("sum", self._part)
+        take_rho()
+        for k in range(n_steps):
+            self._field_chain(e, table[k, 0:2], None)   # Poisson, E, diagnostics, level mats
+            last = k + 1 == n_steps
+            if v_events is not None:
+                v_events[k][0].record(torch.cuda.current_stream())
+            if last:
+                self._fused_step_deferred(e, final=True, mom_out3=self._part[n:])
+                if v_events is not None:
+                    v_events[k][1].record(torch.cuda.current_stream())
+                yield ("sum", self._part[n:])
+            else:
+                self._fused_step_deferred(e)
+                if v_events is not None:
+                    v_events[k][1].record(torch.cuda.current_stream())
+                self._fold_partials(True)
+                yield ("sum", self._part)
+                take_rho()
+            _capi.check(lib.sldg_gather_index(self._part.data_ptr(), self._mom_idx.data_ptr(),
+                                              3, table[k, 2:5].data_ptr(), current_stream()))
+        return table
 
     def advance(self, n_steps: int, table=None, v_events=None):
         """n_steps pipelined Strang steps on this rank's tiles; row k of the returned
@@ -449,28 +640,7 @@ class PencilShardedSimulation(Simulation):
         import torch
         if table is None:
             table = torch.empty((n_steps, 5), dtype=torch.float64, device=self._f.device)
-        if n_steps == 0:
-            return table
-        e = self._e
-        n = self._f.shape[1]
-        # leading half x-step of step 0 on my tiles, rho summed over the ranks
-        self._fused_step_deferred(e, mode=2)
-        self._take_sums(self._reducer(self._fold_partials(False).clone()))
-        for k in range(n_steps):
-            self._field_chain(e, table[k, 0:2], None)   # Poisson, E, diagnostics, level mats
-            if v_events is not None:
-                v_events[k][0].record(torch.cuda.current_stream())
-            last = k + 1 == n_steps
-            if last:
-                self._fused_step_deferred(e, final=True, mom_out3=self._part[n:])
-                self._part[:n].zero_()
-                table[k, 2:5].copy_(self._reducer(self._part.clone())[n:])
-            else:
-                self._fused_step_deferred(e)
-                self._take_sums(self._reducer(self._fold_partials(True).clone()), table[k, 2:5])
-            if v_events is not None:
-                v_events[k][1].record(torch.cuda.current_stream())
-        return table
+        return self.comm.run(self.advance_steps(n_steps, table, v_events))
 
     def step(self):
         """One Strang step (the pipelined path with n_steps = 1)."""

@@ -528,9 +528,60 @@ def test_slab_tiles_kernel_matches_periodic(p, nx):
         scr = torch.empty(nb.value, dtype=torch.uint8, device=DEV)
         rho = torch.empty(nl * o, dtype=torch.float64, device=DEV)
         _capi.check(_capi.lib().sldg_advect_x_slab_tiles(
-            sim.x_plan.device_handle(), e_d.data_ptr(), width, lw - hl * o, hl, nl,
-            out.data_ptr(), width, lw, w.data_ptr(), None, None, None, None, rho.data_ptr(),
-            scr.data_ptr(), current_stream()))
+            sim.x_plan.device_handle(), e_d.data_ptr(), width, lw - hl * o, hl, hr, nl,
+            out.data_ptr(), width, lw, 1, 0, fg.shape[0], 0, w.data_ptr(), None, None, None,
+            None, rho.data_ptr(), scr.data_ptr(), current_stream()))
+        got = out[:, lw:lw + nl * o].cpu().numpy()
+        ref = full[:, c0 * o:(c0 + nl) * o].cpu().numpy()
+        assert np.array_equal(got, ref), (c0, nl)
+        r_ref = sim.vweights @ ref
+        assert np.abs(rho.cpu().numpy() - r_ref).max() <= 1e-13 * np.abs(r_ref).max()
+
+
+@pytest.mark.parametrize("p,nx", [(2, 32), (3, 24)])
+def test_slab_xx_kernel_matches_periodic_xx(p, nx):
+    """n_apply = 2 on a slab (doubled halos, the intermediate's halo cells formed in the
+    kernel) == the periodic X.X pass on the slab's columns, bitwise, in row chunks whose
+    rho / moments accumulate in call order."""
+    import ctypes as C
+
+    from paper_2603_19959_b200 import _capi
+    from paper_2603_19959_b200._device import current_stream
+    from paper_2603_19959_b200.xfield import advect_x_fused_into
+    cfg = sv.SimConfig(dim=3, n_base=4, levels=1, degree=p, n_x=nx, degree_x=2, n_steps=1)
+    sim = sv.Simulation(cfg)
+    o = sim.xgrid.degree + 1
+    rng = np.random.default_rng(nx * p)
+    fg = rng.standard_normal(tuple(sim.f.shape))
+    full = torch.empty_like(sim.f)
+    advect_x_fused_into(dev(fg), full, sim.x_plan, 2)
+    hl1, hr1 = sim.x_plan.halo()
+    hl, hr = max(2, 2 * hl1), max(1, 2 * hr1)
+    w = dev(sim.vweights)
+    n_rows = fg.shape[0]
+    cut = (n_rows // (p + 1) ** 3 // 2) * (p + 1) ** 3
+    for c0, nl in ((0, 12), (nx - 12, 12), (5, 13)):
+        if max(hl, hr) > nl:
+            continue
+        lw, rw = hl * o + (hl * o) % 2, hr * o + (hr * o) % 2
+        width = lw + nl * o + rw
+        width += width & 1
+        ext = np.zeros((n_rows, width))
+        cells = [(c0 - hl + k) % nx for k in range(hl + nl + hr)]
+        ext[:, lw - hl * o:lw + (nl + hr) * o] = np.concatenate(
+            [fg[:, c * o:(c + 1) * o] for c in cells], axis=1)
+        e_d = dev(ext)
+        out = torch.zeros_like(e_d)
+        nb = C.c_size_t()
+        _capi.check(_capi.lib().sldg_advect_x_slab_tiles_scratch(
+            sim.x_plan.device_handle(), nl, width, C.byref(nb)))
+        scr = torch.empty(nb.value, dtype=torch.uint8, device=DEV)
+        rho = torch.empty(nl * o, dtype=torch.float64, device=DEV)
+        for i, (r0, r1) in enumerate(((0, cut), (cut, n_rows))):
+            _capi.check(_capi.lib().sldg_advect_x_slab_tiles(
+                sim.x_plan.device_handle(), e_d.data_ptr(), width, lw - hl * o, hl, hr, nl,
+                out.data_ptr(), width, lw, 2, r0, r1 - r0, i, w.data_ptr(), None, None, None,
+                None, rho.data_ptr(), scr.data_ptr(), current_stream()))
         got = out[:, lw:lw + nl * o].cpu().numpy()
         ref = full[:, c0 * o:(c0 + nl) * o].cpu().numpy()
         assert np.array_equal(got, ref), (c0, nl)

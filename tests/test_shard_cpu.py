@@ -1,10 +1,11 @@
-"""Multi-rank x-slab logic on CPU: world_size 2 (and 3) over gloo.
+"""Multi-rank host logic of the sharded steps on CPU: world_size 2 and 3 over gloo.
 
-The device kernels cannot run here, so the slab x-update is evaluated with the
-oracle's 1D SLDG math, indexed exactly like the CUDA slab kernel
-(xfield.cu k_advect_x, slab mode: source cell = cell + halo_l - n).  What is
-under test is the product's host logic: partition, halo widths, the P2P
-exchange into the margins, the rho all-gather and the rank-order sums.
+The device kernels cannot run here, so the per-row halo pack / unpack is restated on
+the host (the layout of csrc/halo.cu) and the two device reductions are replaced by
+host stand-ins inside the worker processes.  What is under test is the product's
+exchange layer, shard.Collectives.run servicing an advance() generator's requests:
+the P2P halo exchange on the periodic ring into the margins, the rho all-gather in rank
+order, the rank-order sum; plus the slab partition and the pencil item ranges.
 """
 import os
 import socket
@@ -15,7 +16,6 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from oracle import sldg_oracle as so
 from paper_2603_19959_b200 import shard
 
 
@@ -27,78 +27,87 @@ def free_port():
     return p
 
 
-def slab_update(ext, hl, n_local, o, groups_per_row):
-    """Oracle math on a margin buffer: out[cell] = A u[cell+hl-n] + B u[cell+hl-n-1]."""
-    n_rows = ext.shape[0]
-    out = np.empty((n_rows, n_local * o))
-    for r in range(n_rows):
-        n, a, A, B = groups_per_row[r]
-        u = ext[r].reshape(-1, o)
-        if n == 0 and a == 0.0:
-            out[r] = u[hl:hl + n_local].ravel()
-            continue
-        for c in range(n_local):
-            out[r, c * o:(c + 1) * o] = A @ u[c + hl - n] + B @ u[c + hl - n - 1]
+def _np_ordered_sum(parts, out):
+    acc = parts[0].clone()
+    for p in parts[1:]:
+        acc += p
+    out.copy_(acc)
     return out
 
 
-def _worker(rank, world, port, nx, p, speeds, f_glob, result_q):
+def _np_gather_index(src, idx, out):
+    out.copy_(src[idx])
+    return out
+
+
+def _widths(rng, n_rows, reach):
+    """Per-row upwind halo widths like halo.cu: one side per row (or none)."""
+    side = rng.integers(0, 3, n_rows)            # 0 identity, 1 left-reaching, 2 right
+    w = rng.integers(1, reach + 1, n_rows)
+    return np.where(side == 1, w, 0), np.where(side == 2, w, 0)
+
+
+def _worker(rank, world, port, f_glob, nx, o, wl, wr, result_q):
+    """One rank: its slab of f_glob in a [margin | local | margin] buffer; the per-row
+    upwind halo packed on the host (the layout of halo.cu), exchanged by
+    Collectives.run, unpacked by the 'after' callback; then an all-gather of a rho
+    segment and a rank-order sum, all through the product's Collectives."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        o = p + 1
-        xg = so.XGrid(nx, p, 4.0 * np.pi)
-        dt = 0.05
+        shard.ordered_sum = _np_ordered_sum          # device kernels -> host stand-ins
+        shard.gather_index = _np_gather_index
         part = shard.SlabPartition(nx, world)
         nl, c0 = part.local(rank), part.start(rank)
-        hl, hr = shard.x_halo_cells(xg.h, speeds, dt)
-        ex = shard.HaloExchanger(rank, world, hl, hr, o, nl)
-        width = ex.lw + nl * o + ex.rw
-        buf = torch.zeros((len(speeds), width), dtype=torch.float64)
-        buf[:, ex.lw:ex.lw + nl * o] = torch.from_numpy(f_glob[:, c0 * o:(c0 + nl) * o])
-        ex.exchange(buf)
-        b = buf.numpy()
-        # halo margins must equal the periodic neighbours' cells
-        for k in range(hl):
-            gc = (c0 - hl + k) % nx
-            np.testing.assert_array_equal(b[:, ex.lw - hl * o + k * o:ex.lw - hl * o + (k + 1) * o],
-                                          f_glob[:, gc * o:(gc + 1) * o])
-        for k in range(hr):
-            gc = (c0 + nl + k) % nx
-            s0 = ex.lw + nl * o + k * o
-            np.testing.assert_array_equal(b[:, s0:s0 + o], f_glob[:, gc * o:(gc + 1) * o])
-        groups = []
-        for sp in speeds:
-            n, a = so.split_shift(float(sp), dt, xg.h)
-            A, B = so.overlap_mats(xg.basis, a)
-            groups.append((n, a, A, B))
-        ext = b[:, ex.lw - hl * o:ex.lw + (nl + hr) * o]
-        out = slab_update(ext, hl, nl, o, groups)
-        # rho all-gather and the rank-order sum
-        w = np.linspace(0.5, 1.5, len(speeds))
-        rho_loc = torch.from_numpy(w @ out)
-        rho = shard.allgather_segments(rho_loc, [n * o for n in part.counts()])
-        tot = shard.sum_in_rank_order(torch.tensor([float(out.sum()), float(rank), 1.0]))
-        result_q.put((rank, c0, out, rho.numpy(), tot.numpy(), (hl, hr)))
+        hl, hr = int(wl.max()), int(wr.max())
+        lw, rw = shard.margin_dofs(hl, o), shard.margin_dofs(hr, o)
+        n_rows = f_glob.shape[0]
+        buf = np.zeros((n_rows, lw + nl * o + rw))
+        buf[:, lw:lw + nl * o] = f_glob[:, c0 * o:(c0 + nl) * o]
+        to_r = torch.from_numpy(np.concatenate(
+            [buf[r, lw + (nl - wl[r]) * o:lw + nl * o] for r in range(n_rows)]))
+        to_l = torch.from_numpy(np.concatenate([buf[r, lw:lw + wr[r] * o] for r in range(n_rows)]))
+        fr_l, fr_r = torch.empty_like(to_r), torch.empty_like(to_l)
+
+        def unpack():
+            ol = orr = 0
+            for r in range(n_rows):
+                a, b = wl[r] * o, wr[r] * o
+                buf[r, lw - a:lw] = fr_l.numpy()[ol:ol + a]
+                buf[r, lw + nl * o:lw + nl * o + b] = fr_r.numpy()[orr:orr + b]
+                ol += a
+                orr += b
+
+        seg = shard.SegmentIndex([n * o for n in part.counts()], "cpu")
+        loc = torch.zeros(seg.max_width, dtype=torch.float64)
+        loc[:nl * o] = torch.arange(c0 * o, (c0 + nl) * o, dtype=torch.float64)
+        rho = torch.empty(nx * o, dtype=torch.float64)
+        vec = torch.tensor([1.5 * rank, float(rank), 1.0], dtype=torch.float64)
+
+        def gen():
+            ev = yield ("halo", (to_r, to_l, fr_l, fr_r), unpack)
+            assert ev is None                       # CPU tensors: synchronous
+            yield ("allgather", loc, rho, seg)
+            yield ("sum", vec)
+            return "done"
+
+        assert shard.Collectives(rank, world).run(gen()) == "done"
+        result_q.put((rank, c0, nl, lw, buf, rho.numpy(), vec.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,nx,p", [(2, 16, 2), (3, 24, 1), (2, 12, 3)])
-def test_sharded_x_advection_matches_global(world, nx, p):
+@pytest.mark.parametrize("world,nx,o", [(2, 16, 3), (3, 24, 2), (2, 12, 4)])
+def test_collectives_halo_allgather_sum(world, nx, o):
     rng = np.random.default_rng(world * 100 + nx)
-    speeds = np.concatenate([rng.uniform(-6.0, 6.0, 9), [0.0, 40.0 * 4.0 * np.pi / nx]])
-    xg = so.XGrid(nx, p, 4.0 * np.pi)
-    hl, hr = shard.x_halo_cells(xg.h, speeds, 0.05)
-    if max(hl, hr) > nx // world:
-        speeds = speeds[:-1]
-    f_glob = rng.standard_normal((len(speeds), nx * (p + 1)))
-    ref = so.advect_x(f_glob.copy(), so.x_plan(xg, speeds, 0.05), nx)
+    n_rows = 20
+    f_glob = rng.standard_normal((n_rows, nx * o))
+    wl, wr = _widths(rng, n_rows, nx // world)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, nx, p, speeds, f_glob, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, f_glob, nx, o, wl, wr, q))
              for r in range(world)]
     for pr in procs:
         pr.start()
@@ -106,28 +115,27 @@ def test_sharded_x_advection_matches_global(world, nx, p):
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    res.sort()
-    o = p + 1
-    got = np.concatenate([r[2] for r in res], axis=1)
-    # slab update with exchanged halos == global periodic update, bit for bit
-    # (same operands, same order: python matmul on the same blocks)
-    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-14 * np.abs(ref).max())
-    w = np.linspace(0.5, 1.5, len(speeds))
-    for r in res:
-        np.testing.assert_allclose(r[3], w @ got, rtol=1e-13)
-        assert r[4][1] == sum(range(world)) and r[4][2] == world
-    assert res[0][5][0] >= 1
+    for rank, c0, nl, lw, buf, rho, vec in res:
+        for r in range(n_rows):   # margins hold the periodic neighbours' cells
+            for k in range(wl[r]):
+                gc = (c0 - wl[r] + k) % nx
+                np.testing.assert_array_equal(buf[r, lw - (wl[r] - k) * o:lw - (wl[r] - k - 1) * o],
+                                              f_glob[r, gc * o:(gc + 1) * o])
+            for k in range(wr[r]):
+                gc = (c0 + nl + k) % nx
+                s0 = lw + (nl + k) * o
+                np.testing.assert_array_equal(buf[r, s0:s0 + o], f_glob[r, gc * o:(gc + 1) * o])
+        np.testing.assert_array_equal(rho, np.arange(nx * o, dtype=float))
+        assert vec[0] == sum(1.5 * r for r in range(world)) and vec[2] == world
 
 
-def test_partition_and_halo_widths():
+def test_partition_and_margins():
     p = shard.SlabPartition(10, 4)
     assert p.counts() == [3, 3, 2, 2] and p.start(2) == 6 and sum(p.counts()) == 10
     h = 4.0 * np.pi / 512
     hl, hr = shard.x_halo_cells(h, np.linspace(-6, 6, 145), 0.05)
     # cfg5 grid: max |v| dt/2 / h = 6*0.05/0.0245 = 12.2 cells
     assert hl == 13 and hr == 13
-    with pytest.raises(ValueError):
-        shard.HaloExchanger(0, 2, 5, 1, 3, 4)
     assert shard.margin_dofs(3, 3) == 10 and shard.margin_dofs(2, 3) == 6
 
 
