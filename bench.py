@@ -314,12 +314,62 @@ def run_ours(args):
                            "kernel_ms": sweep_alone_ms},
         "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e,
     }
+    if not args.no_amr:
+        # the AMR configurations of the scaling claim (BASELINE configs 4 and 5), each on
+        # all N GPUs (x-slab sharding, the same global problem at every N: strong scaling)
+        del sim
+        torch.cuda.empty_cache()
+        out["amr_scaling"] = {c: time_amr(c, world, rank, args.amr_steps, sv, args.amr_slab1)
+                              for c in args.amr_configs.split(",") if c}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_1core(args.config)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out))
+
+
+def time_amr(config, world, rank, steps, sv, slab1=False):
+    """ms per Strang step of `config` on `world` GPUs: Simulation at N = 1, x-slab
+    ShardedSimulation (NCCL halo exchange overlapped with the X.X pass) at N > 1.
+    CUDA events on the launching stream after 2 warm-up steps, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    cfg = sv.SimConfig(**CONFIGS[config], n_steps=steps)
+    t0 = time.perf_counter()
+    if world > 1 or slab1:
+        from paper_2603_19959_b200.shard import ShardedSimulation
+        sim = ShardedSimulation(cfg, rank, world)
+        par = f"x-slab x{world}" + (" (sharded path)" if world == 1 else "")
+    else:
+        sim = sv.Simulation(cfg)
+        par = "x-slab x1"
+    setup_s = time.perf_counter() - t0
+    sim.advance(2)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    table = sim.advance(steps)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    n_v = len(sim.vweights)
+    dofs = n_v * sim.xgrid.n_dofs
+    fin = bool(torch.isfinite(table).all().item())
+    del sim
+    torch.cuda.empty_cache()
+    return {"workload": NAMES[config], "n_gpus": world, "scaling": "strong",
+            "parallelism": par, "phase_dofs": dofs, "steps": steps, "warmup": 2,
+            "ms_per_step": ms, "value": dofs / (ms * 1e-3), "unit": UNIT,
+            "setup_s": setup_s, "records_finite": fin,
+            "timing": "CUDA events around advance(steps) on the launching stream, max over ranks"}
 
 
 class CpuSteps:
@@ -410,6 +460,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-amr", action="store_true",
+                    help="skip the AMR scaling lines (configs 4 and 5 on the same N GPUs)")
+    ap.add_argument("--amr-configs", default="cfg4,cfg5")
+    ap.add_argument("--amr-steps", type=int, default=10)
+    ap.add_argument("--amr-slab1", action="store_true",
+                    help="at N = 1 run the AMR lines through the sharded (x-slab) path")
     ap.add_argument("--cpu-budget", type=float, default=240.0,
                     help="reference arm: seconds for warm-up + timed steps before the "
                          "warm-up is cut to one step")
