@@ -74,3 +74,99 @@ def test_config5_x_sampled_rows(cfg5):
     ref = so.advect_x(before.copy(), so.x_plan(xg, sim.vcoords[rows, 0], 0.5 * sim.config.dt),
                       512)
     assert np.abs(after - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def _closed_pencils(ps, seeds):
+    """Pencils whose union is closed under sharing a weighted cell (every contribution to
+    a weighted target is inside the set), starting from `seeds`."""
+    owners = {}
+    for q in range(ps.n_pencils):
+        for c in ps.cell_ids[ps.span(q)]:
+            owners.setdefault(int(c), []).append(q)
+    todo, have = list(seeds), set()
+    while todo:
+        q = todo.pop()
+        if q in have:
+            continue
+        have.add(q)
+        for c in ps.cell_ids[ps.span(q)]:
+            todo.extend(p for p in owners[int(c)] if p not in have)
+    return sorted(have)
+
+
+def _sub_plan(oplan, pencils, n_local):
+    """The plan restricted to `pencils` (plan order kept), DOFs renumbered compactly."""
+    keep = set(pencils)
+    cells = set()
+    groups = []
+    per = None
+    for g in oplan.groups:
+        per = g.gather.shape[0] // len(g.pencils)
+        sel = [i for i, q in enumerate(g.pencils) if q in keep]
+        if not sel:
+            continue
+        rows = np.concatenate([np.arange(i * per, (i + 1) * per) for i in sel])
+        groups.append((g, rows))
+        cells.update((g.gather[rows] // n_local).ravel().tolist())
+    cell_list = np.array(sorted(cells), dtype=np.int64)
+    dof = (cell_list[:, None] * n_local + np.arange(n_local)[None, :]).ravel()
+    new = []
+    for g, rows in groups:
+        gat = np.searchsorted(dof, g.gather[rows])
+        new.append(so.Group(g.lowers, g.widths, g.levels, g.conforming, gat, g.weights[rows],
+                            [q for q in g.pencils if q in keep]))
+    return so.Plan(oplan.basis, oplan.radius, oplan.base_width, oplan.n_levels, len(dof),
+                   new), dof
+
+
+@pytest.mark.slow
+def test_config5_full_steps_sampled(cfg5):
+    """Whole Strang steps at config 5 (pipelined advance(), the path run() uses), checked
+    from the GPU's own state at steps 1 and 3 (restarting each check from the device
+    state): E against the oracle's rho (all 3M rows, streamed in chunks) -> Poisson; the
+    coefficients of a closed set of pencils through the refined core (every weighted
+    target's contributions inside the set) against the oracle's X/2 -> V -> X/2 on
+    those rows with the device's E."""
+    sim, oplan = cfg5
+    m = sim.mesh
+    om = so.Mesh(m.dim, m.radius, m.n_base, m.levels, m.lo, m.width)
+    ops = so.mark_conforming(so.make_pencils(om, 0), sim.config.bc)
+    o3 = (sim.config.degree + 1) ** 3
+    # seeds: pencils through the finest cells
+    fine = np.nonzero(ops.levels == ops.levels.max())[0]
+    q_of = np.searchsorted(ops.offsets, fine, side="right") - 1
+    pencils = _closed_pencils(ops, [int(q_of[0]), int(q_of[len(q_of) // 2])])
+    sub, rows = _sub_plan(oplan, pencils, o3)
+    assert len(sub.groups) >= 1 and any((g.weights != 1.0).any() for g in sub.groups)
+    xg = so.XGrid(512, 2, sim.config.length)
+    dt = sim.config.dt
+    poisson = so.Poisson(xg)
+    w = sim.vweights
+    done = 0
+    for target in (1, 3):
+        if target - 1 > done:
+            sim.advance(target - 1 - done)
+            done = target - 1
+        # oracle rho of X/2(f), all rows in chunks (row-local x shifts)
+        rho = np.zeros(xg.n_dofs)
+        n_rows = sim.f.shape[0]
+        step_rows = 27 * 8192
+        for r0 in range(0, n_rows, step_rows):
+            r1 = min(n_rows, r0 + step_rows)
+            blk = sim.f[r0:r1].cpu().numpy()
+            so.advect_x(blk, so.x_plan(xg, sim.vcoords[r0:r1, 0], 0.5 * dt), 512)
+            rho += w[r0:r1] @ blk
+        e_ref = poisson.efield(poisson.solve(rho))
+        f0 = sim.f[torch.from_numpy(rows).to(sim.f.device)].cpu().numpy()
+        sim.advance(1)
+        done = target
+        e_gpu = sim._e.cpu().numpy()
+        assert np.abs(e_gpu - e_ref).max() <= 1e-12 * np.abs(e_ref).max()
+        ref = so.advect_x(f0, so.x_plan(xg, sim.vcoords[rows, 0], 0.5 * dt), 512)
+        so.advect_v(ref, e_gpu, dt, sub, sim.config.bc, workers=8)
+        so.advect_x(ref, so.x_plan(xg, sim.vcoords[rows, 0], 0.5 * dt), 512)
+        got = sim.f[torch.from_numpy(rows).to(sim.f.device)].cpu().numpy()
+        scale = np.abs(ref).max()
+        assert np.abs(got - ref).max() <= 1e-12 * scale, target
+        big = np.abs(ref) >= 1e-3 * scale
+        assert (np.abs(got - ref)[big] / np.abs(ref)[big]).max() <= 1e-12, target
