@@ -479,24 +479,40 @@ k_writeback(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fou
   }
   if (__ldg(speeds + c) != 0.0) {   // exact-zero speed: untouched bits
     int g = s_grp[0];
-    for (int k = 0; k < nk; ++k) {
-      const bool sh = k < kWbMaxC;
-      const int gk = sh ? s_grp[k] : P.c_group[k0 + k];
-      if (gk != g) {
+    // contributions in batches of KB: every slot value of the batch is loaded before
+    // the ordered sum consumes them (KB x RPT independent loads in flight per thread)
+    constexpr int KB = 4;
+    for (int kb = 0; kb < nk; kb += KB) {
+      double rv[KB][RPT];
 #pragma unroll
-        for (int rr = 0; rr < RPT; ++rr) {
-          o[rr] = __dadd_rn(o[rr], sm[rr]);
-          sm[rr] = 0.0;
-        }
-        g = gk;
+      for (int j = 0; j < KB; ++j) {
+        const int k = kb + j;
+        const bool live = k < nk;
+        const double* src = !live ? nullptr
+                            : (k < kWbMaxC ? s_src[k]
+                                           : acc + (long long)P.c_slot[k0 + k] * NLOC * n_cols) + c;
+#pragma unroll
+        for (int rr = 0; rr < RPT; ++rr)
+          rv[j][rr] = (live && r0 + rr < NLOC) ? __ldcs(src + (long long)(r0 + rr) * n_cols) : 0.0;
       }
-      const double* src = (sh ? s_src[k] : acc + (long long)P.c_slot[k0 + k] * NLOC * n_cols) + c;
-      const double wk = sh ? s_w[k] : P.c_weight[k0 + k];
 #pragma unroll
-      for (int rr = 0; rr < RPT; ++rr) {
-        const int r = r0 + rr;
-        const double rv = (r < NLOC) ? src[(long long)r * n_cols] : 0.0;
-        sm[rr] = __dadd_rn(sm[rr], __dmul_rn(wk, __dsub_rn(rv, fv[rr])));
+      for (int j = 0; j < KB; ++j) {
+        const int k = kb + j;
+        if (k >= nk) break;
+        const bool sh = k < kWbMaxC;
+        const int gk = sh ? s_grp[k] : P.c_group[k0 + k];
+        if (gk != g) {
+#pragma unroll
+          for (int rr = 0; rr < RPT; ++rr) {
+            o[rr] = __dadd_rn(o[rr], sm[rr]);
+            sm[rr] = 0.0;
+          }
+          g = gk;
+        }
+        const double wk = sh ? s_w[k] : P.c_weight[k0 + k];
+#pragma unroll
+        for (int rr = 0; rr < RPT; ++rr)
+          sm[rr] = __dadd_rn(sm[rr], __dmul_rn(wk, __dsub_rn(rv[j][rr], fv[rr])));
       }
     }
 #pragma unroll
