@@ -38,17 +38,34 @@ def to_device_f64(a, contiguous=True):
 
 
 class Scratch:
-    """Grow-only device byte buffer cache keyed by name."""
+    """Grow-only device byte buffer cache keyed by name.
+
+    Once a CUDA graph has captured launches that use these buffers (`pin()`, called by
+    Simulation.advance_graph), a buffer that has to grow is retired instead of freed, so
+    a replayed graph never writes into memory the allocator handed to another tensor.
+    Entries keyed by an object's id are dropped when the object is collected
+    (`release_with`)."""
 
     def __init__(self):
         self._bufs = {}
+        self._retired = []
+        self._pinned = False
+
+    def pin(self):
+        self._pinned = True
+
+    def _replace(self, name, buf):
+        old = self._bufs.get(name)
+        if old is not None and self._pinned:
+            self._retired.append(old)
+        self._bufs[name] = buf
 
     def get(self, name, nbytes):
         nbytes = max(int(nbytes), 256)
         buf = self._bufs.get(name)
         if buf is None or buf.numel() < nbytes or buf.device != device():
             buf = torch.empty(nbytes, dtype=torch.uint8, device=device())
-            self._bufs[name] = buf
+            self._replace(name, buf)
         return buf
 
     def like(self, name, t: torch.Tensor):
@@ -56,8 +73,19 @@ class Scratch:
         buf = self._bufs.get(name)
         if buf is None or buf.shape != t.shape or buf.device != t.device:
             buf = torch.empty_like(t)
-            self._bufs[name] = buf
+            self._replace(name, buf)
         return buf
+
+    def drop(self, key):
+        """Forget the entries of `key` (a name, or the id-tagged names (tag, key))."""
+        for name in [n for n in self._bufs if n == key or (isinstance(n, tuple) and n[1:] == (key,))]:
+            if not self._pinned:
+                del self._bufs[name]
+
+    def release_with(self, obj):
+        """Drop the entries keyed by id(obj) when obj is garbage collected."""
+        import weakref
+        weakref.finalize(obj, self.drop, id(obj))
 
 
 SCRATCH = Scratch()

@@ -172,7 +172,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     for (int k = 0; k < kFRing; ++k) mbar_init(&full[k], 1);
     mbar_fence_init();
   }
-  __syncthreads();
+  sync_fz();
 
   const bool per = (bc == SLDG_BC_PERIODIC);
   const bool colv = tid < n_cols;
@@ -226,7 +226,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
   auto stage_sync = [&](int st, int b, long long it) {
     stage(st, b, it);
     cp_async_wait_all();
-    __syncthreads();
+    sync_fz();
   };
 
   // item 0 tables, synchronously
@@ -248,7 +248,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
       atomicMax(&s_nsmax[L], nsi);
     }
   }
-  __syncthreads();
+  sync_fz();
 
   // ---- ring of cell tiles: one load sequence across the CTA's items.  Item i's
   // loads are the cells first..last of its segment (sb-1..se, wrapped when
@@ -576,7 +576,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     // per barrier (copies issued after barrier k complete before barrier k + 1)
     auto tile_barrier = [&]() {
       if (n_staged > 0 && n_staged <= 3) cp_async_wait_all();
-      __syncthreads();
+      sync_fz();
       if (has_next && n_staged < 3) stage(n_staged, b ^ 1, it + 1);
       ++n_staged;
     };
@@ -605,7 +605,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     if (has_next && n_staged < 4) {
       // finish the next item's prefetch when this segment was too short to hide it
       if (n_staged >= 1) cp_async_wait_all();
-      __syncthreads();
+      sync_fz();
       for (int st = n_staged; st < 3; ++st) stage_sync(st, b ^ 1, it + 1);
     }
   }
@@ -619,17 +619,17 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
 #pragma unroll
     for (int k = 0; k < OX; ++k) red[iv * n_cols + cx * OX + k] = rha[k];
   }
-  __syncthreads();
+  sync_fz();
   if (colv) {
     double s = 0.0;
     for (int k = 0; k < OV; ++k) s += red[k * n_cols + c];
     fa.rho_part[(long long)c * gridDim.x + blockIdx.x] = s;
   }
-  __syncthreads();
+  sync_fz();
   red[tid] = m0;
   red[nthr + tid] = m1;
   red[2 * nthr + tid] = m2;
-  __syncthreads();
+  sync_fz();
   if (tid < 3) {
     double s = 0.0;
     for (int k = 0; k < nthr; ++k) s += red[tid * nthr + k];
@@ -886,6 +886,7 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
       for (int of = 16; of > 0; of >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, of);
       if (lane == 0) mom_prev[wp] = sacc;
     }
+    fuzz_delay();
     cluster.sync();
     for (int c = tid; c < nd; c += blockDim.x) {
       if (c >= c0 && c < c1) continue;
@@ -937,6 +938,7 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
       phi[row] = t;
     }
   }
+  fuzz_delay();
   cluster.sync();
   for (int node = tid; node < nn; node += blockDim.x) {
     if (node >= q0 && node < q1) continue;
@@ -960,6 +962,7 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
     e_s[k] = t;
     e[k] = t;
   }
+  fuzz_delay();
   cluster.sync();
   if (rank == 0) {
     // field diagnostics (k_field_diag): max |E| and 0.5 w.E^2, 1024-slot trees
@@ -1019,6 +1022,7 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
     for (int k = 0; k < O * O; ++k)
       lm_mats[((long long)(lev * 2 + ab) * O * O + k) * nd + c] = M[k];
   }
+  fuzz_delay();
   cluster.sync();   // no CTA leaves while another may still read its shared memory
 }
 

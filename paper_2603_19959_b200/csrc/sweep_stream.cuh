@@ -60,7 +60,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     for (int k = 0; k < kStreamRing; ++k) mbar_init(&full[k], 1);
     mbar_fence_init();
   }
-  __syncthreads();
+  sync_fz();
   const bool colv = tid < tx;
   const long long c = c0 + tid;
   const double speed = colv ? __ldg(speeds + c) : 0.0;
@@ -70,7 +70,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     atomicMin(&s_nsmin, nsi);
     atomicMax(&s_nsmax, nsi);
   }
-  __syncthreads();
+  sync_fz();
   const bool streamable = (s_nsmin >= -1 && s_nsmax <= 0) || (s_nsmin > s_nsmax);
 
   double A[O * O], B[O * O];
@@ -193,7 +193,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
         }
       }
     }
-    __syncthreads();   // slot of virtual cell s-1 is refilled next iteration
+    sync_fz();   // slot of virtual cell s-1 is refilled next iteration
   }
 }
 

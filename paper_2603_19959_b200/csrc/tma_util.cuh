@@ -3,6 +3,30 @@
 
 namespace sldg {
 
+// Schedule fuzzing (the race check that stands in for compute-sanitizer, which the GPU
+// pool does not allow): built with -DSLDG_FUZZ (tools/fuzz_build.sh -> libsldg_fuzz.so),
+// every bulk-copy issue, cp.async issue, mbarrier wait and pipeline barrier first sleeps a
+// pseudo-random 0-2 us on ~1 in 4 calls, so producers and consumers of each shared buffer
+// run far out of their usual order; tests/test_gpu_schedule_fuzz.py then requires
+// bit-identical results.  Compiles to nothing otherwise.
+__device__ __forceinline__ void fuzz_delay() {
+#ifdef SLDG_FUZZ
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  unsigned x = (unsigned)c ^ (threadIdx.x * 2654435761u) ^ (blockIdx.x * 40503u) ^
+               (unsigned)(c >> 32);
+  x ^= x >> 13;
+  x *= 0x5bd1e995u;
+  x ^= x >> 15;
+  if ((x & 3u) == 0u) __nanosleep((x >> 4) & 2047u);
+#endif
+}
+// __syncthreads with a fuzzed arrival (a pipeline barrier)
+__device__ __forceinline__ void sync_fz() {
+  fuzz_delay();
+  __syncthreads();
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
@@ -18,6 +42,7 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
                : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  fuzz_delay();
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -32,6 +57,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // completion counted in transaction bytes on `bar`
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
                                          unsigned long long* bar) {
+  fuzz_delay();
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
           "r"(smem_u32(dst)),
@@ -48,14 +74,17 @@ __device__ __forceinline__ void grid_dep_launch() {
 }
 // per-thread asynchronous global -> shared copies (LDGSTS), completed by cp_async_wait_all
 __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  fuzz_delay();
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
 }
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  fuzz_delay();
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
 }
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  fuzz_delay();
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src)
                : "memory");
 }

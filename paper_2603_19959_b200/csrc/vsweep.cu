@@ -34,6 +34,7 @@
 
 #include "sldg_common.cuh"
 #include "plans.cuh"
+#include "tma_util.cuh"
 
 namespace sldg {
 
@@ -402,7 +403,10 @@ k_vitems(VPlanDev P, DevBasis b, const double* __restrict__ fin, double* __restr
   const unsigned nc = (unsigned)n_cols;
   for (;;) {
     unsigned u = 0;
-    if (lane == 0) u = atomicAdd(cnt + 2, 1u);
+    if (lane == 0) {
+      fuzz_delay();
+      u = atomicAdd(cnt + 2, 1u);
+    }
     u = __shfl_sync(~0u, u, 0);
     if (u >= n_units) break;
     const bool slow = u < n_slow;

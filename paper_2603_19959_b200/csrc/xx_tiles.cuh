@@ -97,7 +97,7 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     for (int k = 0; k < nring; ++k) mbar_init(&full[k], need_meta ? 33 : 1);
     mbar_fence_init();
   }
-  __syncthreads();
+  sync_fz();
 
   const int g0 = blockIdx.x, gs = gridDim.x;
   const int my = g0 < n_groups ? (n_groups - g0 + gs - 1) / gs : 0;
@@ -239,7 +239,7 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
           }
         }
       }
-      __syncthreads();
+      sync_fz();
       src = md;
     }
     if (live) {
@@ -263,7 +263,7 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
         }
       }
     }
-    __syncthreads();                          // slot s and mid are reused next
+    sync_fz();                          // slot s and mid are reused next
     if (++s == nring) {
       s = 0;
       phase ^= 1;
@@ -278,13 +278,13 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
 #pragma unroll
       for (int k = 0; k < OX; ++k) red[tt * row_len + cx * OX + k] = rha[k];
     }
-    __syncthreads();
+    sync_fz();
     for (int e = tid; e < row_len; e += blockDim.x) {
       double v = 0.0;
       for (int q = 0; q < tpc; ++q) v += red[q * row_len + e];
       epi.rho_part[(long long)blockIdx.x * row_len + e] = v;
     }
-    __syncthreads();
+    sync_fz();
   }
   if (mom) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0;
@@ -300,7 +300,7 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     red[tid] = s0;
     red[blockDim.x + tid] = s1;
     red[2 * blockDim.x + tid] = s2;
-    __syncthreads();
+    sync_fz();
     if (tid < 3) {
       double v = 0.0;
       for (int q = 0; q < (int)blockDim.x; ++q) v += red[tid * blockDim.x + q];

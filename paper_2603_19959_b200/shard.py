@@ -388,6 +388,8 @@ class ShardedSimulation:
         _capi.check(_capi.lib().sldg_advect_x_slab_tiles_scratch(
             self.x_plan.device_handle(), self.n_local, self.width, C.byref(nb)), ValueError)
         self._xscratch = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+        from ._device import SCRATCH
+        SCRATCH.release_with(self.sweep_plan)
         self.t = 0.0
 
     def fused_step_supported(self) -> bool:

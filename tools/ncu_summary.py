@@ -46,8 +46,11 @@ def launches(path):
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    if path.endswith(".csv"):   # an `ncu -i ... --page raw --csv` dump made on the GPU box
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
     res = []
@@ -77,11 +80,11 @@ def main():
         cfg = sys.argv[sys.argv.index("--config") + 1]
     args = [a for a in sys.argv[2:] if not a.startswith("--") and a != cfg]
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    if args and args[0].endswith(".csv"):
+    if args and args[0].endswith(".csv") and not args[0].endswith("_raw.csv"):
         txt = launches(args[0])
         open(os.path.join(ROOT, "profiles", f"{tag}_launches.txt"), "w").write(txt + "\n")
         print(txt)
-    rep = [a for a in args if a.endswith(".ncu-rep")]
+    rep = [a for a in args if a.endswith(".ncu-rep") or a.endswith("_raw.csv")]
     if rep:
         res = full(rep[0])
         lines = []
