@@ -322,6 +322,8 @@ int sldg_outer(const double* a, int64_t na, const double* b, int64_t nb, double*
                void* stream);
 const char* sldg_last_error(void);
 int sldg_version(void);
+/* bit 0: schedule-fuzzing build (-DSLDG_FUZZ, libsldg_fuzz.so; tests only) */
+int sldg_build_flags(void);
 /* number of kernel launches enqueued by this library since load (for bench) */
 int64_t sldg_launch_count(void);
 

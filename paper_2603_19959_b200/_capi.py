@@ -70,6 +70,7 @@ _lib = None
 
 _SIGS = {
     "sldg_version": (C.c_int, []),
+    "sldg_build_flags": (C.c_int, []),
     "sldg_last_error": (C.c_char_p, []),
     "sldg_launch_count": (C.c_int64, []),
     "sldg_step_fused_query": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,

@@ -138,6 +138,15 @@ const char* sldg_last_error(void) { return g_last_error.c_str(); }
 
 int sldg_version(void) { return 10000; }
 
+// bit 0: built with -DSLDG_FUZZ (schedule fuzzing, tests only)
+int sldg_build_flags(void) {
+#ifdef SLDG_FUZZ
+  return 1;
+#else
+  return 0;
+#endif
+}
+
 int64_t sldg_launch_count(void) { return (int64_t)g_launches.load(); }
 
 int sldg_outer(const double* a, int64_t na, const double* b, int64_t nb, double* out, int64_t ld,

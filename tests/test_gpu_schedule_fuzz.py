@@ -68,6 +68,7 @@ def test_results_survive_schedule_fuzzing():
             "import test_gpu_schedule_fuzz as t; "
             "from paper_2603_19959_b200 import _capi; "
             "assert _capi.LIB_PATH.endswith('libsldg_fuzz.so'); "
+            "assert _capi.lib().sldg_build_flags() & 1; "
             "print(json.dumps(t.digests()))") % (ROOT, os.path.join(ROOT, "tests"))
     for _ in range(2):
         res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True,
@@ -79,4 +80,6 @@ def test_results_survive_schedule_fuzzing():
 
 def test_digests_are_deterministic():
     os.environ.setdefault("SLDG_FUSED", "force")
+    from paper_2603_19959_b200 import _capi
+    assert _capi.lib().sldg_build_flags() == 0   # the product library never fuzzes
     assert digests() == digests()
