@@ -336,7 +336,7 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     for (int r = 0; r < R; ++r) out[r * rw] = me[r * n_cols];
   };
   // 1-D periodic shift of the x cells of one row by the x-speed's (A, B): cell
-  // sources ua (cell - n) and ub (cell - n - 1), same arithmetic as k_xadv
+  // sources ua (cell - n) and ub (cell - n - 1), same arithmetic as k_xx_tiles / k_advect_x
   auto xmul = [&](const double* xa, const double* xb, const double* ua, const double* ub, double* y) {
 #pragma unroll
     for (int k = 0; k < OX; ++k) {

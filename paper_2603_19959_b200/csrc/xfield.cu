@@ -92,7 +92,6 @@ k_advect_x(XPlanDev X, const double* __restrict__ fin, long long ld_in, double* 
 
 }  // namespace sldg
 
-#include "xadv_kernel.cuh"
 
 namespace sldg {
 
@@ -337,124 +336,6 @@ static int launch_advect_x(const sldg_xplan* X, const double* fin, long long ld_
   return SLDG_OK;
 }
 
-struct XadvGeom {
-  int wpb, grid, cpcm;
-  bool tab_smem;
-  size_t smem;
-  bool ok;
-};
-
-// Geometry depends only on the problem shape (never on the variant or the
-// device), so every variant shares one row->warp->CTA partition and the
-// fused reductions are bitwise reproducible.
-// Rows of 8 x (power of two <= 32) cells with a shared-memory speed table use
-// the specialised k_xadv_c (compile-time chunk of 8 cells).
-// chunk length of the specialised kernel for this plan: 8, 16, or 0 (not eligible)
-static int xadv_c_eligible(const sldg_xplan* X) {
-  const long long n = X->n_cells;
-  if (X->o < 2 || X->o > 4) return 0;
-  if (X->n_speeds * 2 * X->o * X->o * sizeof(double) > 32 * 1024) return 0;
-  for (int cpc : {8}) {   // the 16-cell variant measured slower than k_xadv (r01 profiles)
-    if (n % cpc != 0) continue;
-    const long long l = n / cpc;
-    if (l >= 1 && l <= 32 && (l & (l - 1)) == 0) return cpc;
-  }
-  return 0;
-}
-
-static XadvGeom xadv_geom(const sldg_xplan* X, int napply, bool rho, bool allow_c = true) {
-  (void)napply;
-  (void)rho;
-  XadvGeom g;
-  g.tab_smem = X->n_speeds * 2 * X->o * X->o * sizeof(double) <= 32 * 1024;
-  XGeom G = x_geom((int)X->n_cells, X->o, X->n_speeds, g.tab_smem, 1 << 30);
-  g.cpcm = G.cpc <= 8 ? 8 : (G.cpc <= 16 ? 16 : 0);
-  int shared_dbl = G.shared_dbl, per_warp = G.per_warp, rpw = G.rpw;
-  const int cpc = allow_c ? xadv_c_eligible(X) : 0;
-  if (cpc) {
-    g.cpcm = -cpc;   // marks the specialised kernel
-    XcGeom C;
-    const int n = (int)X->n_cells;
-    switch (X->o * 100 + cpc) {
-      case 208: C = xc_geom<2, 8>(n, X->n_speeds); break;
-      case 308: C = xc_geom<3, 8>(n, X->n_speeds); break;
-      case 408: C = xc_geom<4, 8>(n, X->n_speeds); break;
-      case 216: C = xc_geom<2, 16>(n, X->n_speeds); break;
-      case 316: C = xc_geom<3, 16>(n, X->n_speeds); break;
-      default: C = xc_geom<4, 16>(n, X->n_speeds); break;
-    }
-    shared_dbl = C.shared_dbl;
-    per_warp = C.per_warp;
-    rpw = C.rpw;
-  }
-  G.shared_dbl = shared_dbl;
-  G.per_warp = per_warp;
-  G.rpw = rpw;
-  const size_t budget = 227 * 1024 - 1024;
-  int best_w = 1, best_warps = 0;
-  for (int w = 1; w <= 8; ++w) {
-    size_t smem = sizeof(double) * ((size_t)G.shared_dbl + (size_t)w * G.per_warp);
-    if (smem > budget) break;
-    int ctas = (int)std::min<size_t>(budget / smem, 8);
-    if (ctas * w >= best_warps) {
-      best_warps = ctas * w;
-      best_w = w;
-    }
-  }
-  g.wpb = best_w;
-  g.smem = sizeof(double) * ((size_t)G.shared_dbl + (size_t)g.wpb * G.per_warp);
-  g.ok = g.smem <= budget && g.cpcm != 0;
-  const int ctas_per_sm = g.ok ? (int)std::max<size_t>(1, std::min<size_t>(8, budget / g.smem)) : 1;
-  long long groups = (X->n_rows + G.rpw - 1) / G.rpw;
-  long long want = (groups + g.wpb - 1) / g.wpb;
-  g.grid = (int)std::max<long long>(1, std::min<long long>(want, 148LL * ctas_per_sm));
-  return g;
-}
-
-template <int O, int NAPPLY, bool MOM, bool RHO>
-static int launch_xadv_t(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
-                         long long ld_out, const XEpi& epi, const XadvGeom& g, bool vec,
-                         cudaStream_t st) {
-  if (g.cpcm < 0) {
-    auto kc = g.cpcm == -8 ? k_xadv_c<O, NAPPLY, MOM, RHO, 8> : k_xadv_c<O, NAPPLY, MOM, RHO, 16>;
-    SLDG_CUDA_TRY(smem_limit((const void*)kc, (int)std::max<size_t>(g.smem, 48 * 1024)));
-    kc<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
-                                           (int)X->n_cells, (int)X->n_speeds, epi);
-    SLDG_LAUNCH_CHECK("k_xadv_c");
-    return SLDG_OK;
-  }
-  auto k = g.cpcm == 8 ? k_xadv<O, NAPPLY, MOM, RHO, 8> : k_xadv<O, NAPPLY, MOM, RHO, 16>;
-  SLDG_CUDA_TRY(smem_limit((const void*)k, (int)std::max<size_t>(g.smem, 48 * 1024)));
-  k<<<g.grid, 32 * g.wpb, g.smem, st>>>(X->dev, fin, ld_in, fout, ld_out, X->n_rows,
-                                        (int)X->n_cells, (int)X->n_speeds, g.tab_smem ? 1 : 0,
-                                        epi);
-  SLDG_LAUNCH_CHECK("k_xadv");
-  return SLDG_OK;
-}
-
-template <int O>
-static int launch_xadv(const sldg_xplan* X, const double* fin, long long ld_in, double* fout,
-                       long long ld_out, int napply, bool mom, bool rho, const XEpi& epi,
-                       const XadvGeom& g, cudaStream_t st) {
-  if (!g.ok) {
-    set_error("x row too long for the pipelined x kernel");
-    return SLDG_ERR_UNSUPPORTED;
-  }
-  const bool vec = true;
-  int key = (napply == 2 ? 4 : 0) | (mom ? 2 : 0) | (rho ? 1 : 0);
-  switch (key) {
-    case 0: return launch_xadv_t<O, 1, false, false>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
-    case 1: return launch_xadv_t<O, 1, false, true>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
-    case 2: return launch_xadv_t<O, 1, true, false>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
-    case 3: return launch_xadv_t<O, 1, true, true>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
-    case 4: return launch_xadv_t<O, 2, false, false>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
-    case 5: return launch_xadv_t<O, 2, false, true>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
-    case 6: return launch_xadv_t<O, 2, true, false>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
-    case 7: return launch_xadv_t<O, 2, true, true>(X, fin, ld_in, fout, ld_out, epi, g, vec, st);
-  }
-  return SLDG_ERR_ARG;
-}
-
 }  // namespace sldg
 
 #include "xx_tiles.cuh"
@@ -541,14 +422,6 @@ static int launch_xt(const sldg_xplan* X, const XTGeom& g, const double* fin, do
   }
   set_error("x tile kernel: unsupported degrees");
   return SLDG_ERR_UNSUPPORTED;
-}
-
-// 16-byte-aligned rows: the specialised kernel is allowed (its geometry then fixes the
-// row partition of every pass on these buffers)
-static bool xadv_vec(const sldg_xplan* X, const double* fin, const double* fout, long long ld_in,
-                     long long ld_out) {
-  return ((X->n_cells * X->o) % 2 == 0) && (ld_in % 2 == 0) && (ld_out % 2 == 0) &&
-         ((((unsigned long long)fin) & 15) == 0) && ((((unsigned long long)fout) & 15) == 0);
 }
 
 }  // namespace sldg
@@ -722,18 +595,12 @@ int sldg_advect_x(const sldg_xplan* X, const double* fin, double* fout, int64_t 
     XTGeom tg = xt_geom(X);
     if (tg.ok) return launch_xt(X, tg, fin, fout, ld, 1, false, false, epi, st);
   }
+  // rows without the velocity-cell layout (1V, or a plan built for arbitrary rows):
+  // the generic row kernel
   switch (X->o) {
-#define CASE(O)                                                                     \
-  case O:                                                                           \
-    if (xadv_geom(X, 1, false).ok)                                                  \
-      return launch_xadv<O>(X, fin, ld, fout, ld, 1, false, false, epi,            \
-                            xadv_geom(X, 1, false, xadv_vec(X, fin, fout, ld, ld)), st); \
-    return launch_advect_x<O>(X, fin, ld, fout, ld, (int)X->n_cells, (int)X->n_cells, 0, 1, st);
-    CASE(2) CASE(3) CASE(4)
-#undef CASE
 #define CASE(O) \
   case O: return launch_advect_x<O>(X, fin, ld, fout, ld, (int)X->n_cells, (int)X->n_cells, 0, 1, st);
-    CASE(5) CASE(6)
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6)
 #undef CASE
   }
   set_error("unsupported degree");
@@ -745,10 +612,8 @@ int sldg_xadv_scratch_bytes(const sldg_xplan* X, size_t* bytes) {
     set_error("bad argument");
     return SLDG_ERR_ARG;
   }
-  XadvGeom g = xadv_geom(X, 2, true, true), g2 = xadv_geom(X, 2, true, false);
-  XTGeom tg = xt_geom(X);
-  long long grid = std::max(g.grid, g2.grid);
-  if (tg.ok) grid = std::max(grid, tg.grid_);
+  const XTGeom tg = xt_geom(X);
+  const long long grid = tg.ok ? tg.grid_ : 1;
   *bytes = sizeof(double) * (size_t)grid * (3 + X->n_cells * X->o) + 256;
   return SLDG_OK;
 }
@@ -766,40 +631,27 @@ int sldg_advect_x_fused(const sldg_xplan* X, const double* fin, double* fout, in
   }
   if (X->n_rows == 0) return SLDG_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  XadvGeom g = xadv_geom(X, n_apply, rho, xadv_vec(X, fin, fout, ld, ld));
   const XTGeom tg = xt_geom(X);
-  if (tg.ok) g.grid = (int)tg.grid_;   // partials are per CTA of the kernel that runs
+  if (!tg.ok) {   // the caller runs the separate passes (advect_x, rho, moments)
+    set_error("fused x pass: needs the velocity-cell row layout (sldg_xplan_set_vlayout) "
+              "and rows of at most 512 cells");
+    return SLDG_ERR_UNSUPPORTED;
+  }
   XEpi epi{w, v0, v2, xw, nullptr, nullptr};
   if (scratch) {
     epi.mom_part = (double*)scratch;
-    epi.rho_part = (double*)scratch + 3 * (size_t)g.grid;
+    epi.rho_part = (double*)scratch + 3 * (size_t)tg.grid_;
   }
-  int rc = SLDG_ERR_UNSUPPORTED;
-  if (tg.ok) {
-    rc = launch_xt(X, tg, fin, fout, ld, n_apply, mom, rho, epi, st);
-  } else {
-    if (!g.ok) {
-      set_error("fused x pass: row too long for the shared-memory ring");
-      return rc;
-    }
-    switch (X->o) {
-#define CASE(O) \
-  case O: rc = launch_xadv<O>(X, fin, ld, fout, ld, n_apply, mom, rho, epi, g, st); break;
-      CASE(2) CASE(3) CASE(4)
-#undef CASE
-      default:
-        set_error("fused x pass compiled for degree_x <= 3");
-    }
-  }
+  const int rc = launch_xt(X, tg, fin, fout, ld, n_apply, mom, rho, epi, st);
   if (rc) return rc;
   if (mom) {
-    k_sum3<<<1, 96, 0, st>>>(epi.mom_part, g.grid, mom_out3);
+    k_sum3<<<1, 96, 0, st>>>(epi.mom_part, tg.grid_, mom_out3);
     SLDG_LAUNCH_CHECK("k_sum3");
   }
   if (rho) {
     const long long row_len = X->n_cells * X->o;
-    k_colsum<<<(unsigned)((row_len * 32 + 255) / 256), 256, 0, st>>>(epi.rho_part, g.grid, row_len,
-                                                                rho_out);
+    k_colsum<<<(unsigned)((row_len * 32 + 255) / 256), 256, 0, st>>>(epi.rho_part, tg.grid_,
+                                                                row_len, rho_out);
     SLDG_LAUNCH_CHECK("k_colsum");
   }
   return SLDG_OK;

@@ -15,12 +15,22 @@
 //   RHO         : rho = w . f of the final output
 // Per-thread column accumulators; CTA partials in a fixed order; the grid
 // depends only on the problem shape (bitwise-reproducible reductions).
-// Arithmetic per output identical to k_xadv / k_advect_x.
+// Arithmetic per output identical to k_advect_x (the generic row kernel).
 #pragma once
 
 #include "tma_util.cuh"
 
 namespace sldg {
+
+// epilogue operands of the x passes: moments of the (first) result, rho of the final one
+struct XEpi {
+  const double* w;     // velocity quadrature weights (rows)
+  const double* v0;    // v_x per row
+  const double* v2;    // |v|^2 per row
+  const double* xw;    // x quadrature weights (cols)
+  double* mom_part;    // [grid][3]
+  double* rho_part;    // [grid][row_len]
+};
 
 struct XTGeom {
   int rpt, tpc, nring, threads;   // rows per tile, tiles per CTA step, ring depth, threads

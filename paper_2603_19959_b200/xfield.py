@@ -121,7 +121,7 @@ def advect_x_into(f_in, f_out, plan: XAdvectionPlan):
 
 
 def advect_x_fused_into(f_in, f_out, plan: XAdvectionPlan, n_apply=1, mom=None, rho=None):
-    """f_out = X^n_apply(f_in) with fused epilogues (csrc/xfield.cu k_xadv).
+    """f_out = X^n_apply(f_in) with fused epilogues (csrc/xx_tiles.cuh k_xx_tiles).
 
     mom = (w, v0, v2, xw, out3): moments of the state after the first
     application; rho = (w, out): charge density of the final state.  All

@@ -99,7 +99,7 @@ def main():
         summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
         summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
         for key, pat in (("sweep", "k_sweep_stream"), ("step_fused", "k_step_fused"),
-                         ("xx", "k_xadv")):
+                         ("xx", "k_xx_tiles")):
             hits = [d for d in res if pat in d["kernel"]]
             if not hits:
                 continue
