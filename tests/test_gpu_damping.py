@@ -39,7 +39,9 @@ def test_damping_run_matches_reference(name):
     ref = g["records"]
     assert rec.shape == ref.shape
     np.testing.assert_allclose(rec[:, 0], ref[:, 0], rtol=0, atol=1e-12)
-    assert np.abs(rec[:, 1] - ref[:, 1]).max() <= 1e-10 * ref[0, 1]
+    # measured: 2.9e-12 (cfg1), 1.5e-11 (cfg2), 7.7e-14 (cfg3), 2.7e-13 (cfg4) normwise --
+    # the 1e-13 absolute rho difference (rho ~ 1) over E = -phi' of rho - mean(rho)
+    assert np.abs(rec[:, 1] - ref[:, 1]).max() <= 5e-11 * ref[0, 1]
     np.testing.assert_allclose(rec[:, [2, 4, 6]], ref[:, [2, 4, 6]], rtol=1e-12)
     assert res.fit.n_peaks == int(g["n_peaks"])
     assert abs(res.fit.rate - float(g["rate"])) <= 1e-8 * abs(float(g["rate"]))
