@@ -26,7 +26,15 @@ struct VPlanDev {
   const long long* walk_pencils;  // whole-fast pencils, for k_sweep_walk
   const long long* walk_desc;     // per walk position: {p_off, p_n | level << 32}
   const long long* gen_entries;   // entries of the per-cell worklist when walk is used
-  long long n_entries, n_targets, n_walk, n_gen;
+  // duplicate pencils (identical cell lists, whole-fast, every cell in exactly those
+  // pencils): the walk sweeps one representative and writes the weighted average of the
+  // identical results directly (the write-back formula, no scratch slots)
+  const int* e_dd;                // entry -> dedup weight list (-1: none)
+  const long long* dd_off;        // dedup list -> first weight
+  const double* dd_w;             // weights of the duplicates, plan order
+  const long long* walk_dd;       // the walk without the skipped duplicates
+  const long long* t_dd;          // targets the write-back still owns in dedup mode
+  long long n_entries, n_targets, n_walk, n_gen, n_walk_dd, n_targets_dd;
   int stride_d, stride_t0, stride_t1;
   int n_levels;
   double radius, base_width;
@@ -39,6 +47,7 @@ struct sldg_vplan {
   sldg::VPlanDev dev;
   int dim, direction, o, n_lines, n_local;
   long long n_cells, n_pencils, n_entries, n_slots, n_targets, n_walk, n_gen, n_dofs;
+  long long n_dd_sets, n_walk_dd, n_targets_dd;
   int max_pencil_cells, max_walk_cells;
   void* block;
 };

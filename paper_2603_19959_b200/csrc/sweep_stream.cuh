@@ -34,7 +34,8 @@ __global__ void __launch_bounds__(256, 1)
 k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
                long long ld, long long n_cols, const double* __restrict__ speeds, int bc,
                const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
-               double* __restrict__ acc, int tx_max, int n_tiles, int whole_rows) {
+               double* __restrict__ acc, int tx_max, int n_tiles, int whole_rows,
+               const long long* __restrict__ walk, int dedup) {
   constexpr int NL = (DIM == 3) ? O * O : 1;
   constexpr int NLOC = NL * O;
   extern __shared__ __align__(128) double sm[];
@@ -43,7 +44,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
 
   const long long wp = blockIdx.x / n_tiles;
   const int tile = (int)(blockIdx.x - wp * n_tiles);
-  const long long q = P.walk_pencils[wp];
+  const long long q = walk[wp];
   const long long off = P.p_off[q];
   const int n = P.p_n[q];
   const long long c0 = (long long)tile * tx_max;
@@ -75,13 +76,23 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
 
   double A[O * O], B[O * O];
   if (colv) load_pair<O>(lm_mats, lev, n_cols, c, A, B);
+  // the weighted write-back of a deduplicated target (k_writeback's arithmetic for
+  // identical contributions y): fv + ((0 + w1 (y - fv)) + w2 (y - fv) + ...)
+  auto dd_value = [&](int dd, double y, double fv) -> double {
+    const long long k0 = P.dd_off[dd], k1 = P.dd_off[dd + 1];
+    const double df = __dsub_rn(y, fv);
+    double sm = 0.0;
+    for (long long k = k0; k < k1; ++k) sm = __dadd_rn(sm, __dmul_rn(__ldg(P.dd_w + k), df));
+    return __dadd_rn(fv, sm);
+  };
 
   if (!streamable) {
     // arbitrary shifts in this tile: direct loads from HBM (same arithmetic)
     if (!colv) return;
     for (int s = 0; s < n; ++s) {
       const long long e = off + s;
-      const int slot = P.e_slot[e];
+      const int dd = dedup ? P.e_dd[e] : -1;
+      const int slot = dd >= 0 ? -1 : P.e_slot[e];
       double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c : acc + (long long)slot * NLOC * n_cols + c;
       const long long dstride = slot < 0 ? ld : n_cols;
       const double* self = fin + P.e_row0[e] * ld + c;
@@ -105,7 +116,10 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
         }
         two_cell<O>(A, B, ua, ub, va, vb, y);
 #pragma unroll
-        for (int i = 0; i < O; ++i) dst[(long long)Lines<O, DIM>::row(P, t, i) * dstride] = y[i];
+        for (int i = 0; i < O; ++i) {
+          const long long r = Lines<O, DIM>::row(P, t, i);
+          dst[r * dstride] = dd >= 0 ? dd_value(dd, y[i], self[r * ld]) : y[i];
+        }
       }
     }
     return;
@@ -152,7 +166,8 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     waited = max(waited, khi);
     if (colv) {
       const long long e = off + s;
-      const int slot = P.e_slot[e];
+      const int dd = dedup ? P.e_dd[e] : -1;
+      const int slot = dd >= 0 ? -1 : P.e_slot[e];
       double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c
                              : acc + (long long)slot * NLOC * n_cols + c;
       const long long dstride = slot < 0 ? ld : n_cols;
@@ -181,7 +196,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
 #pragma unroll
             for (int i = 0; i < O; ++i) {
               const int r = (DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i;
-              dst[(long long)r * dstride] = y[i];
+              dst[(long long)r * dstride] = dd >= 0 ? dd_value(dd, y[i], me[r * rstride]) : y[i];
             }
           }
         };

@@ -453,13 +453,15 @@ constexpr int kWbRows = 4;    // rows per thread
 template <int NLOC, int RPT>
 __global__ void __launch_bounds__(128)
 k_writeback(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout, long long ld,
-            long long n_cols, const double* __restrict__ speeds, const double* __restrict__ acc) {
+            long long n_cols, const double* __restrict__ speeds, const double* __restrict__ acc,
+            const long long* __restrict__ tlist) {
   constexpr int NRG = (NLOC + RPT - 1) / RPT;
   __shared__ const double* s_src[kWbMaxC];   // acc row 0 of each contribution's slot
   __shared__ int s_grp[kWbMaxC];
   __shared__ double s_w[kWbMaxC];
-  const long long t = blockIdx.x / NRG;
-  const int r0 = (int)(blockIdx.x - t * NRG) * RPT;
+  const long long tb = blockIdx.x / NRG;
+  const long long t = tlist ? tlist[tb] : tb;   // dedup mode: only the targets left
+  const int r0 = (int)(blockIdx.x - tb * NRG) * RPT;
   const long long k0 = P.t_off[t];
   const int nk = (int)(P.t_off[t + 1] - k0);
   const int ns = min(nk, kWbMaxC);
@@ -609,14 +611,21 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
                      : sched && !std::strcmp(sched, "items") ? false
                                                              : p->n_walk * n_tiles >= num_sms();
   const bool use_stream = !force_slow && p->n_walk > 0 && tx_max > 0 && n_cols >= 2 && fills;
+  // duplicate pencils swept once, their targets written directly (SLDG_SWEEP_DEDUP=0 off)
+  static const bool dd_off = [] {
+    const char* e = std::getenv("SLDG_SWEEP_DEDUP");
+    return e && e[0] == '0';
+  }();
+  const bool dedup = use_stream && p->n_dd_sets > 0 && !dd_off;
   if (use_stream) {
     const int threads = (tx_max + 31) / 32 * 32;
     const int rstride = whole ? (int)ld : tx_max;
     const size_t smem = sizeof(double) * (size_t)kStreamRing * NLOC * rstride;
     SLDG_CUDA_TRY(smem_limit((const void*)k_sweep_stream<O, DIM>, (int)smem));
-    const long long blocks = p->n_walk * n_tiles;
+    const long long blocks = (dedup ? p->n_walk_dd : p->n_walk) * n_tiles;
     k_sweep_stream<O, DIM><<<(unsigned)blocks, threads, smem, st>>>(
-        p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, tx_max, n_tiles, whole);
+        p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, tx_max, n_tiles, whole,
+        dedup ? p->dev.walk_dd : p->dev.walk_pencils, dedup ? 1 : 0);
     SLDG_LAUNCH_CHECK("k_sweep_stream");
   }
   // per-cell entries through the device worklist (classify, then balanced items)
@@ -640,12 +649,13 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
                                                       list_s);
     SLDG_LAUNCH_CHECK("k_vitems");
   }
-  if (p->n_targets > 0) {
+  const long long n_wb = dedup ? p->n_targets_dd : p->n_targets;
+  if (n_wb > 0) {
     constexpr int NRG = (NLOC + kWbRows - 1) / kWbRows;
     const int threads = (int)std::min<long long>(128, (n_cols + 31) / 32 * 32);
-    const dim3 grid((unsigned)(p->n_targets * NRG), (unsigned)((n_cols + threads - 1) / threads));
+    const dim3 grid((unsigned)(n_wb * NRG), (unsigned)((n_cols + threads - 1) / threads));
     k_writeback<NLOC, kWbRows><<<grid, threads, 0, st>>>(p->dev, fin, fout, ld, n_cols, speeds,
-                                                          acc);
+                                                          acc, dedup ? p->dev.t_dd : nullptr);
     SLDG_LAUNCH_CHECK("k_writeback");
   }
   return SLDG_OK;
@@ -835,6 +845,49 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
   }
   const long long T = (long long)t_row0.size();
   const long long K = (long long)c_slot.size();
+  // Duplicate whole-fast pencils: identical cell lists (a coarse transverse column split by
+  // the global transverse edges of finer cells elsewhere) give bit-identical sweep results,
+  // so when every cell of the set lies in exactly those pencils the weighted write-back
+  // f + sum_k w_k (r_k - f) (vsweep.py:403-409, one group, plan order) can be formed from
+  // ONE sweep of the first pencil.  The walk then skips the others; the write-back keeps
+  // only the targets outside such sets.  (Used when the walk runs; the worklist schedules
+  // and force_slow keep the plain slots.)
+  std::vector<int> e_dd(E, -1);
+  std::vector<long long> dd_off(1, 0), walk_dd;
+  std::vector<double> dd_w;
+  std::vector<unsigned char> skip(P, 0), t_dedup(T, 0);
+  long long n_dd_sets = 0;
+  {
+    std::map<std::vector<long long>, std::vector<long long>> sets;
+    for (long long q : walk)
+      sets[std::vector<long long>(d->cell_ids + p_off[q], d->cell_ids + p_off[q] + p_n[q])]
+          .push_back(q);
+    std::map<long long, long long> t_of_cell;
+    for (long long t = 0; t < T; ++t) t_of_cell[t_row0[t] / nloc] = t;
+    for (auto& kv : sets) {
+      const std::vector<long long>& qs = kv.second;   // plan order (walk order)
+      const long long dn = (long long)qs.size();
+      if (dn < 2) continue;
+      bool full = true;
+      for (long long cid : kv.first) full = full && cover[cid] == dn;
+      if (!full) continue;
+      ++n_dd_sets;
+      const long long rep = qs[0];
+      for (int s = 0; s < p_n[rep]; ++s) {
+        e_dd[p_off[rep] + s] = (int)(dd_off.size() - 1);
+        for (long long q : qs) dd_w.push_back(d->weights[p_off[q] + s]);
+        dd_off.push_back((long long)dd_w.size());
+        t_dedup[t_of_cell.at(kv.first[s])] = 1;
+      }
+      for (size_t j = 1; j < qs.size(); ++j) skip[qs[j]] = 1;
+    }
+  }
+  for (long long q : walk)
+    if (!skip[q]) walk_dd.push_back(q);
+  std::vector<long long> t_dd;
+  for (long long t = 0; t < T; ++t)
+    if (!t_dedup[t]) t_dd.push_back(t);
+  if (dd_w.empty()) dd_w.push_back(0.0);
 
   // one device allocation, carved
   struct Piece {
@@ -864,6 +917,11 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
       {walk.data(), sizeof(long long) * walk.size(), (void**)&p->dev.walk_pencils},
       {walk_desc.data(), sizeof(long long) * walk_desc.size(), (void**)&p->dev.walk_desc},
       {gen.data(), sizeof(long long) * gen.size(), (void**)&p->dev.gen_entries},
+      {e_dd.data(), sizeof(int) * E, (void**)&p->dev.e_dd},
+      {dd_off.data(), sizeof(long long) * dd_off.size(), (void**)&p->dev.dd_off},
+      {dd_w.data(), sizeof(double) * dd_w.size(), (void**)&p->dev.dd_w},
+      {walk_dd.data(), sizeof(long long) * walk_dd.size(), (void**)&p->dev.walk_dd},
+      {t_dd.data(), sizeof(long long) * t_dd.size(), (void**)&p->dev.t_dd},
   };
   size_t total = 0;
   for (auto& pc : pieces) total = align_up(total + pc.bytes, 256);
@@ -901,6 +959,9 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
   p->n_targets = T;
   p->n_walk = (long long)walk.size();
   p->n_gen = (long long)gen.size();
+  p->n_dd_sets = n_dd_sets;
+  p->n_walk_dd = (long long)walk_dd.size();
+  p->n_targets_dd = (long long)t_dd.size();
   p->n_dofs = d->n_cells * nloc;
   p->max_pencil_cells = max_cells;
   p->max_walk_cells = max_walk;
@@ -916,6 +977,8 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
   p->dev.n_targets = T;
   p->dev.n_walk = p->n_walk;
   p->dev.n_gen = p->n_gen;
+  p->dev.n_walk_dd = p->n_walk_dd;
+  p->dev.n_targets_dd = p->n_targets_dd;
   p->dev.n_levels = d->n_levels;
   p->dev.radius = d->radius;
   p->dev.base_width = d->base_width;
