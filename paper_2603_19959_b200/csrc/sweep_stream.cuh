@@ -179,8 +179,11 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
         // sources: virtual cells s - ns (same) and s - ns - 1 (neighbour); both in
         // the pencil unless an absorbing end cuts one off (first / last cell only)
         const int va_cell = s - (int)ns, vb_cell = s - (int)ns - 1;
-        auto apply = [&](bool va, bool vb, auto checked) {
+        // DD: a deduplicated target (uniform over the CTA: one entry), a separate
+        // instantiation so the common path keeps its unrolled loads
+        auto apply = [&](bool va, bool vb, auto checked, auto dedup_t) {
           constexpr bool CK = decltype(checked)::value;
+          constexpr bool DD = decltype(dedup_t)::value;
           const double* sa = sm + (unsigned)((va ? va_cell : s) - v0) % kStreamRing * cell_dbl + tid;
           const double* sb = sm + (unsigned)((vb ? vb_cell : s) - v0) % kStreamRing * cell_dbl + tid;
 #pragma unroll
@@ -196,15 +199,27 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
 #pragma unroll
             for (int i = 0; i < O; ++i) {
               const int r = (DIM == 3) ? (t % O) * P.stride_t0 + (t / O) * P.stride_t1 + i * P.stride_d : i;
-              dst[(long long)r * dstride] = dd >= 0 ? dd_value(dd, y[i], me[r * rstride]) : y[i];
+              if constexpr (DD)
+                dst[(long long)r * dstride] = dd_value(dd, y[i], me[r * rstride]);
+              else
+                dst[(long long)r * dstride] = y[i];
             }
           }
         };
-        if (per || (va_cell >= 0 && va_cell < n && vb_cell >= 0 && vb_cell < n)) {
-          apply(true, true, std::integral_constant<bool, false>{});
+        using F = std::integral_constant<bool, false>;
+        using T = std::integral_constant<bool, true>;
+        const bool inner = per || (va_cell >= 0 && va_cell < n && vb_cell >= 0 && vb_cell < n);
+        const bool va = va_cell >= 0 && va_cell < n, vb = vb_cell >= 0 && vb_cell < n;
+        if (dd < 0) {
+          if (inner)
+            apply(true, true, F{}, F{});
+          else
+            apply(va, vb, T{}, F{});
         } else {
-          apply(va_cell >= 0 && va_cell < n, vb_cell >= 0 && vb_cell < n,
-                std::integral_constant<bool, true>{});
+          if (inner)
+            apply(true, true, F{}, T{});
+          else
+            apply(va, vb, T{}, T{});
         }
       }
     }

@@ -1,12 +1,14 @@
 #!/bin/bash
-# Build libsldg from the step_fused.cu of git revision $1 as _lib/libsldg_$2.so (the rest of
-# the sources from the working tree), for same-box A/B timing: SLDG_LIB_VARIANT=$2.
+# Build libsldg with the files $3.. (default step_fused.cu) of git revision $1 as
+# _lib/libsldg_$2.so (the rest of the sources from the working tree), for same-box A/B
+# timing: SLDG_LIB_VARIANT=$2.
 set -e
 cd "$(dirname "$0")/.."
-rev=$1; name=$2
+rev=$1; name=$2; shift 2
+files=("$@"); [ ${#files[@]} -eq 0 ] && files=(step_fused.cu)
 tmp=$(mktemp -d)
 cp -r paper_2603_19959_b200/csrc/. "$tmp/"
-git show "$rev:paper_2603_19959_b200/csrc/step_fused.cu" > "$tmp/step_fused.cu"
+for f in "${files[@]}"; do git show "$rev:paper_2603_19959_b200/csrc/$f" > "$tmp/$f"; done
 objs=()
 for f in "$tmp"/*.cu; do
   o="$tmp/$(basename "$f").o"
