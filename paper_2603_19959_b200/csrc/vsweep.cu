@@ -612,10 +612,8 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
                                                              : p->n_walk * n_tiles >= num_sms();
   const bool use_stream = !force_slow && p->n_walk > 0 && tx_max > 0 && n_cols >= 2 && fills;
   // duplicate pencils swept once, their targets written directly (SLDG_SWEEP_DEDUP=0 off)
-  static const bool dd_off = [] {
-    const char* e = std::getenv("SLDG_SWEEP_DEDUP");
-    return e && e[0] == '0';
-  }();
+  const char* dd_env = std::getenv("SLDG_SWEEP_DEDUP");
+  const bool dd_off = dd_env && dd_env[0] == '0';
   const bool dedup = use_stream && p->n_dd_sets > 0 && !dd_off;
   if (use_stream) {
     const int threads = (tx_max + 31) / 32 * 32;
