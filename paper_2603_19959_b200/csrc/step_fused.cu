@@ -542,8 +542,8 @@ k_step_fused(VPlanDev P, XPlanDev X, const double* __restrict__ fin, double* __r
     };
     // MODE 0: composed x-step of cell s's v_x nodes -> dst (XCS entries per node)
     auto x_compose = [&](int s, double* dst) {
-      if (MODE != 0) return;
-      for (int e0 = tid; e0 < OV * XCL; e0 += nthr) {   // the CTA may have < OV*XCL threads
+      for (int e0 = MODE == 0 ? tid : OV * XCL; e0 < OV * XCL; e0 += nthr) {   // (MODE 0 only;
+                                                        // the CTA may have < OV*XCL threads)
         const int jv = e0 / XCL, e = e0 - jv * XCL;
         int pos;   // padded position of logical entry e
         const double* A = xtab + (long long)T.cg[s * OV + jv] * XM;

@@ -144,3 +144,15 @@ def test_pencil_ranks_in_lockstep_match_simulation(kw, world):
         np.testing.assert_allclose(tt[:, :2], tr[:, :2], rtol=1e-10)
     with pytest.raises(NotImplementedError):
         sims[0].step_host(None)
+
+
+def test_slab_run_driver_matches_lockstep():
+    """ShardedSimulation.advance() at world 1 goes through Collectives.run -- the NCCL
+    driver's CUDA-stream path (halo exchange and unpack on the communication stream, the
+    X.X chunks waiting on their events) -- and gives the lockstep driver's bits."""
+    kw = SLAB_CASES[1]
+    a = shard.ShardedSimulation(sv.SimConfig(**kw, n_steps=3), 0, 1, n_chunks=3)
+    ta = a.advance(3).cpu().numpy()
+    f, tabs, _ = _slab_run(kw, 1, 3)
+    np.testing.assert_array_equal(a.f.cpu().numpy(), f)
+    np.testing.assert_array_equal(ta, tabs[0])
