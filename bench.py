@@ -319,8 +319,14 @@ def run_ours(args):
         # all N GPUs (x-slab sharding, the same global problem at every N: strong scaling)
         del sim
         torch.cuda.empty_cache()
-        out["amr_scaling"] = {c: time_amr(c, world, rank, args.amr_steps, sv, args.amr_slab1)
-                              for c in args.amr_configs.split(",") if c}
+        out["amr_scaling"] = {}
+        for c in (c for c in args.amr_configs.split(",") if c):
+            try:
+                out["amr_scaling"][c] = time_amr(c, world, rank, args.amr_steps, sv,
+                                                 args.amr_slab1)
+            except Exception as exc:   # the headline line must still print
+                out["amr_scaling"][c] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+                torch.cuda.empty_cache()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline_1core(args.config)
     if world > 1:
