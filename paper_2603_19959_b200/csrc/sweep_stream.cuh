@@ -19,6 +19,12 @@
 //
 // Valid when every active column of the tile has n_shift in {-1, 0} (all
 // Landau shifts; checked per tile): cell s then needs cells s-1, s, s+1.
+//
+// Line groups.  A Q3 cell (64 rows) leaves room for only 96 columns in the ring,
+// i.e. 3 warps per SM -- too few to cover the two-cell update's FMA chains and the
+// HBM latency (cfg4L: 7.2 ms for 13 GB).  From Q3 up, StreamGeom::NG = O threads
+// share one column, each taking every O-th of the cell's O^2 lines (same arithmetic per
+// output, so the same bits); they all hold the column's A, B.
 #pragma once
 
 #include <type_traits>
@@ -30,7 +36,14 @@ namespace sldg {
 constexpr int kStreamRing = 4;
 
 template <int O, int DIM>
-__global__ void __launch_bounds__(256, 1)
+struct StreamGeom {
+  static constexpr int NG = (DIM == 3 && O >= 4) ? O : 1;   // divides the O^2 lines
+  static constexpr int MAX_THREADS = NG == 4 ? 384 : 256;     // register budget (no spills)
+  static constexpr int MAX_COLS = MAX_THREADS / NG / 32 * 32;   // column tile cap
+};
+
+template <int O, int DIM>
+__global__ void __launch_bounds__(StreamGeom<O, DIM>::MAX_THREADS, 1)
 k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ fout,
                long long ld, long long n_cols, const double* __restrict__ speeds, int bc,
                const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
@@ -38,6 +51,8 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
                const long long* __restrict__ walk, int dedup) {
   constexpr int NL = (DIM == 3) ? O * O : 1;
   constexpr int NLOC = NL * O;
+  constexpr int NG = StreamGeom<O, DIM>::NG;
+  constexpr int NT = NL / NG;   // lines per thread
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) unsigned long long full[kStreamRing];
   __shared__ int s_nsmin, s_nsmax;
@@ -50,6 +65,9 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
   const long long c0 = (long long)tile * tx_max;
   const int tx = (int)min((long long)tx_max, n_cols - c0);
   const int tid = threadIdx.x;
+  const int tpad = (int)blockDim.x / NG;   // columns per line group (multiple of 32)
+  const int g = tid / tpad;                // line group
+  const int col = tid - g * tpad;
   const int lev = P.e_level[off];
   const int rstride = whole_rows ? (int)ld : tx_max;   // smem row stride (doubles)
   const int cell_dbl = NLOC * rstride;
@@ -62,11 +80,11 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     mbar_fence_init();
   }
   sync_fz();
-  const bool colv = tid < tx;
-  const long long c = c0 + tid;
+  const bool colv = col < tx;
+  const long long c = c0 + col;
   const double speed = colv ? __ldg(speeds + c) : 0.0;
   const long long ns = colv ? lm_ns[(long long)lev * n_cols + c] : 0;
-  if (colv && speed != 0.0) {
+  if (colv && g == 0 && speed != 0.0) {
     const int nsi = (int)max(min(ns, (long long)(1 << 29)), -(long long)(1 << 29));
     atomicMin(&s_nsmin, nsi);
     atomicMax(&s_nsmax, nsi);
@@ -97,7 +115,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
       const long long dstride = slot < 0 ? ld : n_cols;
       const double* self = fin + P.e_row0[e] * ld + c;
       if (speed == 0.0) {
-        for (int r = 0; r < NLOC; ++r) dst[r * dstride] = self[r * ld];
+        for (int r = g; r < NLOC; r += NG) dst[r * dstride] = self[r * ld];
         continue;
       }
       long long qa = s - ns, qb = s - ns - 1;
@@ -106,7 +124,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
       else { va = qa >= 0 && qa < n; vb = qb >= 0 && qb < n; }
       const double* pa = fin + (va ? P.e_row0[off + qa] : 0) * ld + c;
       const double* pb = fin + (vb ? P.e_row0[off + qb] : 0) * ld + c;
-      for (int t = 0; t < NL; ++t) {
+      for (int t = g; t < NL; t += NG) {
         double ua[O], ub[O], y[O];
 #pragma unroll
         for (int i = 0; i < O; ++i) {
@@ -171,10 +189,10 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
       double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c
                              : acc + (long long)slot * NLOC * n_cols + c;
       const long long dstride = slot < 0 ? ld : n_cols;
-      const double* me = sm + ((s - v0) % kStreamRing) * cell_dbl + tid;
+      const double* me = sm + ((s - v0) % kStreamRing) * cell_dbl + col;
       if (speed == 0.0) {
 #pragma unroll 3
-        for (int r = 0; r < NLOC; ++r) dst[r * dstride] = me[r * rstride];
+        for (int r = g; r < NLOC; r += NG) dst[r * dstride] = me[r * rstride];
       } else {
         // sources: virtual cells s - ns (same) and s - ns - 1 (neighbour); both in
         // the pencil unless an absorbing end cuts one off (first / last cell only)
@@ -184,10 +202,11 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
         auto apply = [&](bool va, bool vb, auto checked, auto dedup_t) {
           constexpr bool CK = decltype(checked)::value;
           constexpr bool DD = decltype(dedup_t)::value;
-          const double* sa = sm + (unsigned)((va ? va_cell : s) - v0) % kStreamRing * cell_dbl + tid;
-          const double* sb = sm + (unsigned)((vb ? vb_cell : s) - v0) % kStreamRing * cell_dbl + tid;
+          const double* sa = sm + (unsigned)((va ? va_cell : s) - v0) % kStreamRing * cell_dbl + col;
+          const double* sb = sm + (unsigned)((vb ? vb_cell : s) - v0) % kStreamRing * cell_dbl + col;
 #pragma unroll
-          for (int t = 0; t < NL; ++t) {
+          for (int tt = 0; tt < NT; ++tt) {
+            const int t = g + tt * NG;
             double ua[O], ub[O], y[O];
 #pragma unroll
             for (int i = 0; i < O; ++i) {

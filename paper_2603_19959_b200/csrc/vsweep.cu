@@ -588,12 +588,13 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
   const size_t budget = 227 * 1024 - 256;
   const bool al16 = ((((unsigned long long)fin) & 15) == 0) && (ld % 2 == 0);
   int tx_max = 0, whole = 0;
-  if (al16 && n_cols == ld && n_cols <= 256 && (NLOC * n_cols) % 2 == 0 &&
+  constexpr int kMaxCols = StreamGeom<O, DIM>::MAX_COLS;
+  if (al16 && n_cols == ld && (n_cols + 31) / 32 * 32 <= kMaxCols && (NLOC * n_cols) % 2 == 0 &&
       sizeof(double) * kStreamRing * NLOC * n_cols <= budget) {
     tx_max = (int)n_cols;
     whole = 1;
   } else if (al16 && n_cols % 2 == 0) {
-    for (int t = 256; t >= 32; t -= 32)
+    for (int t = kMaxCols; t >= 32; t -= 32)
       if (sizeof(double) * kStreamRing * NLOC * t <= budget) {
         tx_max = t;
         break;
@@ -616,7 +617,7 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
   const bool dd_off = dd_env && dd_env[0] == '0';
   const bool dedup = use_stream && p->n_dd_sets > 0 && !dd_off;
   if (use_stream) {
-    const int threads = (tx_max + 31) / 32 * 32;
+    const int threads = (tx_max + 31) / 32 * 32 * StreamGeom<O, DIM>::NG;
     const int rstride = whole ? (int)ld : tx_max;
     const size_t smem = sizeof(double) * (size_t)kStreamRing * NLOC * rstride;
     SLDG_CUDA_TRY(smem_limit((const void*)k_sweep_stream<O, DIM>, (int)smem));
