@@ -10,7 +10,9 @@
 // consecutive rows of f, so a cell tile is (p+1)^dim rows x TX columns: when
 // the tile spans the full row (TX == ld) it is ONE contiguous block and is
 // fetched with ONE cp.async.bulk (the TMA engine, no per-thread address
-// generation); otherwise with one bulk copy per row.  Cells stream in pencil
+// generation); otherwise with ONE 2-D tensor copy (a tensor map over f, box
+// (p+1)^dim rows x TX columns), or one bulk copy per row when no map could be
+// encoded.  Cells stream in pencil
 // order through a 4-slot ring tracked by mbarriers (transaction bytes), two
 // cells ahead of the compute, so every input coefficient is read from HBM
 // exactly once (absorbing bc; periodic re-reads the two wrap cells).  Outputs
@@ -39,7 +41,11 @@ template <int O, int DIM>
 struct StreamGeom {
   static constexpr int NG = (DIM == 3 && O >= 4) ? O : 1;   // divides the O^2 lines
   static constexpr int MAX_THREADS = NG == 4 ? 384 : 256;     // register budget (no spills)
+#ifdef SLDG_STREAM_COLS
+  static constexpr int MAX_COLS = NG > 1 ? SLDG_STREAM_COLS : 256;
+#else
   static constexpr int MAX_COLS = MAX_THREADS / NG / 32 * 32;   // column tile cap
+#endif
 };
 
 template <int O, int DIM>
@@ -48,7 +54,8 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
                long long ld, long long n_cols, const double* __restrict__ speeds, int bc,
                const long long* __restrict__ lm_ns, const double* __restrict__ lm_mats,
                double* __restrict__ acc, int tx_max, int n_tiles, int whole_rows,
-               const long long* __restrict__ walk, int dedup) {
+               const long long* __restrict__ walk, int dedup,
+               const __grid_constant__ CUtensorMap tmap, int use_tmap) {
   constexpr int NL = (DIM == 3) ? O * O : 1;
   constexpr int NLOC = NL * O;
   constexpr int NG = StreamGeom<O, DIM>::NG;
@@ -158,6 +165,11 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
       if (tid == 0) {
         mbar_expect_tx(bar, cell_bytes);
         bulk_g2s(dst, src, cell_bytes, bar);
+      }
+    } else if (use_tmap) {   // the cell tile as ONE 2-D box (NLOC rows x tx_max columns)
+      if (tid == 0) {
+        mbar_expect_tx(bar, (unsigned)(NLOC * tx_max) * 8u);
+        tma_load_2d(dst, &tmap, (int)c0, (int)P.e_row0[off + cell], bar);
       }
     } else {
       if (tid == 0) mbar_expect_tx(bar, cell_bytes);

@@ -1,5 +1,10 @@
-// tma_util.cuh -- mbarrier + cp.async.bulk (TMA engine, 1-D) helpers for sm_100a.
+// tma_util.cuh -- mbarrier + cp.async.bulk (TMA engine, 1-D and 2-D tensor) helpers for
+// sm_100a.
 #pragma once
+
+#include <cuda.h>   // CUtensorMap (the type only; encoded through the runtime's entry point)
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 namespace sldg {
 
@@ -64,6 +69,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA tensor copy of one 2-D box (coordinates: inner column, row) global -> shared,
+// completion counted in transaction bytes on `bar` (the full box: out-of-range
+// elements are zero-filled and counted)
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            unsigned long long* bar) {
+  fuzz_delay();
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
 // programmatic dependent launch: wait for the preceding grid (no-op when the kernel
 // was not launched with programmatic stream serialization) / let the next grid start
 __device__ __forceinline__ void grid_dep_wait() {
@@ -96,6 +113,35 @@ __device__ __forceinline__ void cp_async_wait_all() {
 __device__ __forceinline__ void cp_async_arrive(unsigned long long* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
+}
+
+// Host: encode a 2-D tensor map over a row-major fp64 matrix (rows x ld doubles, the
+// first `inner` columns addressed; columns past `inner` read as zeros), box
+// box_rows x box_cols, no swizzle.  cuTensorMapEncodeTiled comes from the driver via
+// the runtime's entry-point query, so nothing links against libcuda.  False when the
+// driver or the geometry (16-byte aligned base and row pitch, box <= 256) refuses.
+inline bool encode_tmap_2d(CUtensorMap* map, const double* base, long long inner,
+                           long long rows, long long ld, int box_cols, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000,
+                                         cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!encode || ((unsigned long long)base & 15) || (ld * 8) % 16 || box_cols > 256 ||
+      box_rows > 256 || rows >= (1ll << 31) || inner >= (1ll << 31) || (box_cols * 8) % 16)
+    return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 }  // namespace sldg

@@ -622,9 +622,14 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
     const size_t smem = sizeof(double) * (size_t)kStreamRing * NLOC * rstride;
     SLDG_CUDA_TRY(smem_limit((const void*)k_sweep_stream<O, DIM>, (int)smem));
     const long long blocks = (dedup ? p->n_walk_dd : p->n_walk) * n_tiles;
+    // column tiles: one 2-D tensor copy per cell tile (else one bulk copy per row)
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof(tmap));
+    const bool use_tmap =
+        !whole && encode_tmap_2d(&tmap, fin, n_cols, p->n_dofs, ld, tx_max, NLOC);
     k_sweep_stream<O, DIM><<<(unsigned)blocks, threads, smem, st>>>(
         p->dev, fin, fout, ld, n_cols, speeds, bc, lm_ns, lm_mats, acc, tx_max, n_tiles, whole,
-        dedup ? p->dev.walk_dd : p->dev.walk_pencils, dedup ? 1 : 0);
+        dedup ? p->dev.walk_dd : p->dev.walk_pencils, dedup ? 1 : 0, tmap, use_tmap ? 1 : 0);
     SLDG_LAUNCH_CHECK("k_sweep_stream");
   }
   // per-cell entries through the device worklist (classify, then balanced items)
