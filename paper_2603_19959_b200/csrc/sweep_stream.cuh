@@ -155,11 +155,13 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
   const bool per = (bc == SLDG_BC_PERIODIC);
   const int v0 = per ? -1 : 0;
   const int n_load = per ? n + 2 : n;
-  auto issue = [&](int k) {   // called by warp 0 only
+  auto row_of = [&](int k) {   // first f row of list position k
     const int v = v0 + k;
-    const int cell = v < 0 ? n - 1 : (v >= n ? 0 : v);
+    return P.e_row0[off + (v < 0 ? n - 1 : (v >= n ? 0 : v))];
+  };
+  auto issue = [&](int k, long long row0) {   // called by warp 0 only
     double* dst = sm + (k % kStreamRing) * cell_dbl;
-    const double* src = fin + P.e_row0[off + cell] * ld + c0;
+    const double* src = fin + row0 * ld + c0;
     unsigned long long* bar = &full[k % kStreamRing];
     if (whole_rows) {
       if (tid == 0) {
@@ -169,7 +171,7 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     } else if (use_tmap) {   // the cell tile as ONE 2-D box (NLOC rows x tx_max columns)
       if (tid == 0) {
         mbar_expect_tx(bar, (unsigned)(NLOC * tx_max) * 8u);
-        tma_load_2d(dst, &tmap, (int)c0, (int)P.e_row0[off + cell], bar);
+        tma_load_2d(dst, &tmap, (int)c0, (int)row0, bar);
       }
     } else {
       if (tid == 0) mbar_expect_tx(bar, cell_bytes);
@@ -178,15 +180,31 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
         bulk_g2s(dst + r * rstride, src + (long long)r * ld, (unsigned)tx * 8u, bar);
     }
   };
+  // the plan entries the loop needs are loaded one cell ahead (their latency hides
+  // behind a cell's compute): warp 0 the row of the next list position to fetch,
+  // every thread its cell's (row, slot, dedup set)
+  long long next_row = 0;
   if (tid < 32) {
-    for (int k = 0; k < min(3, n_load); ++k) issue(k);
+    for (int k = 0; k < min(3, n_load); ++k) issue(k, row_of(k));
+    if (n_load > 3) next_row = row_of(3);
   }
-  // per-line row offsets (compile-time for direction 0)
+  auto meta = [&](int s, long long& row, int& slot, int& dd) {
+    const long long e = off + s;
+    dd = dedup ? P.e_dd[e] : -1;
+    slot = dd >= 0 ? -1 : P.e_slot[e];
+    row = P.e_row0[e];
+  };
+  long long m_row = 0;
+  int m_slot = -1, m_dd = -1;
+  if (colv) meta(0, m_row, m_slot, m_dd);
   int waited = -1;
   for (int s = 0; s < n; ++s) {
     // prefetch list position of virtual cell s+2
     const int kn = s + 2 - v0;
-    if (tid < 32 && kn < n_load && kn >= 3) issue(kn);
+    if (tid < 32 && kn < n_load && kn >= 3) {
+      issue(kn, next_row);
+      if (kn + 1 < n_load) next_row = row_of(kn + 1);
+    }
     // wait for virtual cells s-1 .. s+1 that exist in the list; the ones below
     // `waited` were waited for at an earlier cell (their slots are refilled only
     // after every thread is past them)
@@ -194,11 +212,11 @@ k_sweep_stream(VPlanDev P, const double* __restrict__ fin, double* __restrict__ 
     for (unsigned k = (unsigned)max(klo, waited + 1); k <= (unsigned)khi; ++k)
       mbar_wait(&full[k % kStreamRing], (k / kStreamRing) & 1u);
     waited = max(waited, khi);
+    const long long row_s = m_row;
+    const int slot = m_slot, dd = m_dd;
+    if (colv && s + 1 < n) meta(s + 1, m_row, m_slot, m_dd);
     if (colv) {
-      const long long e = off + s;
-      const int dd = dedup ? P.e_dd[e] : -1;
-      const int slot = dd >= 0 ? -1 : P.e_slot[e];
-      double* dst = slot < 0 ? fout + P.e_row0[e] * ld + c
+      double* dst = slot < 0 ? fout + row_s * ld + c
                              : acc + (long long)slot * NLOC * n_cols + c;
       const long long dstride = slot < 0 ? ld : n_cols;
       const double* me = sm + ((s - v0) % kStreamRing) * cell_dbl + col;
