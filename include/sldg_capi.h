@@ -129,6 +129,25 @@ int sldg_weighted_writeback(const double* f_in, int64_t n, const int64_t* csr_of
 /* ---------------------------------------------------------------- x side */
 typedef struct sldg_xplan sldg_xplan;
 
+/* One steady-state AMR Strang step body in one HBM pass (csrc/amr_fused.cuh):
+ * f_out = X(X(V(f_in))) -- the v-sweep (as sldg_advect_v with speeds = E) followed by
+ * the trailing half x-step of this step and the leading half x-step of the next --
+ * with mom_out3 = [m0, m1, m2] of the state after the first x half step and
+ * rho_out[n_cols] = rho of f_out.  Replaces the sldg_advect_v + sldg_advect_x_fused
+ * (n_apply 2) pair of Simulation.advance (the reference's vsweep.py:413-441 then
+ * xfield.py:91-104 twice, driver.py:220-240).  Velocity cells the whole-fast walk
+ * does not write directly get the separate kernels.  Query: SLDG_OK and the scratch
+ * size when the plans qualify (3V, direction 0, the x plan's velocity layout,
+ * sldg_xplan_set_vlayout), SLDG_ERR_UNSUPPORTED otherwise. */
+int sldg_amr_step_query(const sldg_vplan* vplan, const sldg_xplan* xplan, int64_t n_cols,
+                        int64_t ld, size_t* scratch_bytes);
+int sldg_amr_step(const sldg_vplan* vplan, const sldg_xplan* xplan, const double* f_in,
+                  double* f_out, int64_t ld, int64_t n_cols, const double* speeds, double dt,
+                  int32_t bc, const double* w, const double* v0, const double* v2,
+                  const double* xw, double* mom_out3, double* rho_out, void* scratch,
+                  void* stream);
+
+
 typedef struct SldgXPlanDesc {
   SldgBasis basis;            /* degree_x basis */
   int64_t n_cells;            /* global x cells (periodic) */

@@ -114,6 +114,12 @@ _SIGS = {
     "sldg_advect_v": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                 C.c_void_p, C.c_double, C.c_int32, C.c_int32, C.c_void_p,
                                 C.c_void_p]),
+    "sldg_amr_step_query": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                      C.POINTER(C.c_size_t)]),
+    "sldg_amr_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                C.c_int64, C.c_void_p, C.c_double, C.c_int32, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p]),
     "sldg_level_matrices": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_double,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "sldg_xplan_create": (C.c_int, [C.POINTER(SldgXPlanDesc), C.POINTER(C.c_void_p)]),

@@ -34,6 +34,11 @@ struct VPlanDev {
   const double* dd_w;             // weights of the duplicates, plan order
   const long long* walk_dd;       // the walk without the skipped duplicates
   const long long* t_dd;          // targets the write-back still owns in dedup mode
+  const long long* walk_dd_desc;  // per walk_dd position: {p_off, p_n | level << 32}
+  // cells whose rows the walk does not write directly (per-cell worklist cells and the
+  // write-back targets of dedup mode), ascending: the one-pass AMR step
+  // (amr_fused.cuh) finishes them with a cell-list x pass
+  const long long* rest_cells;
   long long n_entries, n_targets, n_walk, n_gen, n_walk_dd, n_targets_dd;
   int stride_d, stride_t0, stride_t1;
   int n_levels;
@@ -47,7 +52,7 @@ struct sldg_vplan {
   sldg::VPlanDev dev;
   int dim, direction, o, n_lines, n_local;
   long long n_cells, n_pencils, n_entries, n_slots, n_targets, n_walk, n_gen, n_dofs;
-  long long n_dd_sets, n_walk_dd, n_targets_dd;
+  long long n_dd_sets, n_walk_dd, n_targets_dd, n_rest;
   int max_pencil_cells, max_walk_cells;
   void* block;
 };

@@ -81,6 +81,27 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(map), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+// TMA-engine bulk copy shared -> global (bulk async-group), and its completion:
+// wait_read = the shared source may be reused, wait_all = the writes are done
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* src, unsigned bytes) {
+  fuzz_delay();
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all0() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+// generic-proxy shared-memory writes -> visible to the async proxy (a bulk store)
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 // programmatic dependent launch: wait for the preceding grid (no-op when the kernel
 // was not launched with programmatic stream serialization) / let the next grid start
 __device__ __forceinline__ void grid_dep_wait() {

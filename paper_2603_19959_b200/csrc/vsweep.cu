@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -438,6 +439,7 @@ k_vitems(VPlanDev P, DevBasis b, const double* __restrict__ fin, double* __restr
 }  // namespace sldg
 
 #include "sweep_stream.cuh"
+#include "amr_fused.cuh"
 
 namespace sldg {
 
@@ -665,6 +667,244 @@ static int launch_sweep(const sldg_vplan* p, const double* fin, double* fout, lo
   return SLDG_OK;
 }
 
+// ---- one-pass AMR step (amr_fused.cuh) --------------------------------------------
+
+long long xx_cells_grid(const sldg_xplan* X, long long n_list);   // xfield.cu
+int xx_cells_run(const sldg_xplan* X, double* f, long long ld, const long long* cells,
+                 long long n_list, const double* w, const double* v0, const double* v2,
+                 const double* xw, double* mom_part, double* rho_part, cudaStream_t st);
+
+__global__ void k_amr_fold(const double* __restrict__ part, long long n_parts, long long n,
+                           double* __restrict__ out) {   // out[c] = sum_k part[k][c], fixed order
+  const int lane = threadIdx.x & 31;
+  const long long c = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  if (c >= n) return;
+  double v = 0.0;
+  for (long long k = lane; k < n_parts; k += 32) v += part[k * n + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) out[c] = v;
+}
+
+struct AmrGeom {
+  bool ok;
+  int ncl, cw, ncx, threads;
+  size_t smem;
+  long long units, clusters, xx_grid;
+  ScratchLayout L;
+  size_t o_xcomp, o_xsh, o_mom, o_rho, total;
+};
+
+template <int O, int OX>
+static AmrGeom amr_geom(const sldg_vplan* p, const sldg_xplan* X, long long n_cols, long long ld) {
+  AmrGeom g{};
+  g.ok = false;
+  if (p->dim != 3 || p->direction != 0 || p->dev.stride_d != 1 || X->vo != O || X->o != OX ||
+      n_cols != X->n_cells * OX || ld < n_cols || ld % 2 != 0 || p->n_walk_dd < 1 ||
+      X->n_rows != p->n_dofs || X->n_speeds < 1)
+    return g;
+  const long long n_xc = X->n_cells;
+  for (int ncl = 1; ncl <= 8 && !g.ok; ++ncl) {
+    if (n_xc % ncl) continue;
+    const int ncx = (int)(n_xc / ncl), cw = ncx * OX;
+    const int threads = (std::max(cw, O * ncx) + 31) / 32 * 32;
+    const size_t smem =
+        sizeof(double) * ((size_t)(kAmrRing + 4) * O * cw + 3 * O * XComp<OX>::N);
+    if (cw % 2 || threads > 512 || smem > 227 * 1024 - 1024 ||
+        3 * threads > kAmrRing * O * cw || O * XComp<OX>::N > 2 * threads)
+      continue;
+    g.ncl = ncl;
+    g.ncx = ncx;
+    g.cw = cw;
+    g.threads = threads;
+    g.smem = smem;
+    g.ok = true;
+  }
+  if (!g.ok) return g;
+  g.units = p->n_walk_dd * O * O;
+  auto k = k_amr_fused<O, OX>;
+  if (smem_limit((const void*)k, (int)g.smem) != cudaSuccess) {
+    g.ok = false;
+    return g;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)g.ncl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3((unsigned)g.ncl);
+  cfg.blockDim = dim3((unsigned)g.threads);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, (void*)k, &cfg) != cudaSuccess || nc < 1) {
+    cudaGetLastError();
+    g.ok = false;
+    return g;
+  }
+  g.clusters = std::min<long long>(nc, g.units);
+  g.xx_grid = p->n_rest > 0 ? xx_cells_grid(X, p->n_rest) : 0;
+  if (p->n_rest > 0 && g.xx_grid == 0) {
+    g.ok = false;
+    return g;
+  }
+  g.L = scratch_layout(p, n_cols);
+  size_t off = align_up(g.L.total, 256);
+  g.o_xcomp = off;
+  off = align_up(off + sizeof(double) * XComp<OX>::N * (size_t)X->n_speeds, 256);
+  g.o_xsh = off;   // per entry, per v_x node: x-speed index
+  off = align_up(off + sizeof(int) * O * (size_t)p->n_entries, 256);
+  g.o_mom = off;
+  off = align_up(off + sizeof(double) * 3 * (size_t)(g.clusters * g.ncl + g.xx_grid), 256);
+  g.o_rho = off;
+  off = align_up(off + sizeof(double) * (size_t)n_cols * (size_t)(g.clusters + g.xx_grid), 256);
+  g.total = off;
+  return g;
+}
+
+// the geometry (occupancy query included) once per plan shape and device: the key holds
+// every number amr_geom reads, so a plan reallocated at another shape misses
+template <int O, int OX>
+static AmrGeom amr_geom_cached(const sldg_vplan* p, const sldg_xplan* X, long long n_cols,
+                               long long ld) {
+  static std::mutex mu;
+  static std::map<std::vector<long long>, AmrGeom> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::vector<long long> key = {
+      dev, p->dim, p->direction, p->dev.stride_d, p->o, p->n_local,
+      p->dev.n_levels, p->n_slots, p->n_entries, p->n_walk_dd, p->n_rest, p->n_dofs,
+      X->vo, X->o, X->n_cells, X->n_rows, X->n_speeds, n_cols, ld};
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const AmrGeom g = amr_geom<O, OX>(p, X, n_cols, ld);
+  cache[key] = g;
+  return g;
+}
+
+template <int O, int OX>
+static int amr_step(const sldg_vplan* p, const sldg_xplan* X, const double* fin, double* fout,
+                    long long ld, long long n_cols, const double* speeds, double dt, int bc,
+                    const double* w, const double* v0, const double* v2, const double* xw,
+                    double* mom_out3, double* rho_out, void* scratch, cudaStream_t st,
+                    size_t* bytes) {
+  const AmrGeom g = amr_geom_cached<O, OX>(p, X, n_cols, ld);
+  if (!g.ok) {
+    set_error("one-pass AMR step: unsupported plan / geometry");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  if (bytes) {
+    *bytes = g.total;
+    return SLDG_OK;
+  }
+  constexpr int NLOC = O * O * O;
+  unsigned char* sb = (unsigned char*)scratch;
+  const ScratchLayout& L = g.L;
+  long long* lm_ns = (long long*)(sb + L.ns_off);
+  double* lm_frac = (double*)(sb + L.frac_off);
+  double* lm_mats = (double*)(sb + L.mats_off);
+  double* acc = (double*)(sb + L.acc_off);
+  unsigned* wl_cnt = (unsigned*)(sb + L.cnt_off);
+  unsigned* list_f = (unsigned*)(sb + L.lf_off);
+  unsigned* list_s = (unsigned*)(sb + L.ls_off);
+  double* xcomp = (double*)(sb + g.o_xcomp);
+  int* e_xg = (int*)(sb + g.o_xsh);
+  double* mom_part = (double*)(sb + g.o_mom);
+  double* rho_part = (double*)(sb + g.o_rho);
+  if (L.list_cap >= (long long)kNoItem) {
+    set_error("amr step: entries x columns exceed the 32-bit worklist index");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  int rc = launch_level_mats<O>(p, speeds, n_cols, dt, lm_ns, lm_frac, lm_mats, wl_cnt, st);
+  if (rc) return rc;
+  k_xcomp<OX><<<(unsigned)((X->n_speeds + 127) / 128), 128, 0, st>>>(X->dev, xw, X->n_speeds,
+                                                                     xcomp);
+  SLDG_LAUNCH_CHECK("k_xcomp");
+  k_entry_speeds<O><<<(unsigned)((p->n_entries * O + 255) / 256), 256, 0, st>>>(
+      p->dev, X->dev.row_speed, p->n_entries, e_xg);
+  SLDG_LAUNCH_CHECK("k_entry_speeds");
+  // cells outside the walk: the per-cell worklist (v only), as launch_sweep's walk mode
+  if (p->n_gen > 0) {
+    const long long n = p->n_gen * n_cols;
+    k_vclassify<O, 3><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        p->dev, fin, fout, ld, n_cols, speeds, bc, 0, lm_ns, acc, p->n_gen, 1, wl_cnt, list_f,
+        list_s);
+    SLDG_LAUNCH_CHECK("k_vclassify");
+    using IG = ItemGroups<O, 3>;
+    int per_sm = 0;
+    SLDG_CUDA_TRY(resident_ctas((const void*)k_vitems<O, 3>, 128, IG::SMEM, &per_sm));
+    const long long max_units = (n + 31) / 32 * IG::NG;
+    const long long blocks =
+        std::max<long long>(1, std::min<long long>((long long)std::max(per_sm, 1) * num_sms(),
+                                                   (max_units + 3) / 4));
+    k_vitems<O, 3><<<(unsigned)blocks, 128, IG::SMEM, st>>>(p->dev, p->basis, fin, fout, ld,
+                                                           n_cols, speeds, dt, bc, lm_ns,
+                                                           lm_mats, acc, 1, wl_cnt, list_f,
+                                                           list_s);
+    SLDG_LAUNCH_CHECK("k_vitems");
+  }
+  // the walk: V + X.X in one pass for its direct rows
+  {
+    const AmrEpi ep{w, v0, v2, xcomp, e_xg, mom_part, rho_part};
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)g.ncl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(g.clusters * g.ncl));
+    cfg.blockDim = dim3((unsigned)g.threads);
+    cfg.dynamicSmemBytes = g.smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    SLDG_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_amr_fused<O, OX>, p->dev, fin, fout, ld, (int)n_cols,
+                                     (int)X->n_cells, speeds, bc, (const long long*)lm_ns,
+                                     (const double*)lm_mats, acc, ep, g.units));
+    SLDG_LAUNCH_CHECK("k_amr_fused");
+  }
+  // weighted targets (dedup mode: the ones the walk did not finish)
+  if (p->n_targets_dd > 0) {
+    constexpr int NRG = (NLOC + kWbRows - 1) / kWbRows;
+    const int threads = (int)std::min<long long>(128, (n_cols + 31) / 32 * 32);
+    const dim3 grid((unsigned)(p->n_targets_dd * NRG), (unsigned)((n_cols + threads - 1) / threads));
+    k_writeback<NLOC, kWbRows><<<grid, threads, 0, st>>>(p->dev, fin, fout, ld, n_cols, speeds,
+                                                          acc, p->dev.t_dd);
+    SLDG_LAUNCH_CHECK("k_writeback");
+  }
+  // X.X of the rest, in place, partials after the walk's
+  rc = xx_cells_run(X, fout, ld, p->dev.rest_cells, p->n_rest, w, v0, v2, xw,
+                    mom_part + 3 * g.clusters * g.ncl, rho_part + g.clusters * n_cols, st);
+  if (rc) return rc;
+  k_amr_fold<<<1, 96, 0, st>>>(mom_part, g.clusters * g.ncl + g.xx_grid, 3, mom_out3);
+  SLDG_LAUNCH_CHECK("k_amr_fold");
+  k_amr_fold<<<(unsigned)((n_cols * 32 + 255) / 256), 256, 0, st>>>(
+      rho_part, g.clusters + g.xx_grid, n_cols, rho_out);
+  SLDG_LAUNCH_CHECK("k_amr_fold");
+  return SLDG_OK;
+}
+
+static int amr_dispatch(const sldg_vplan* p, const sldg_xplan* X, const double* fin, double* fout,
+                        long long ld, long long n_cols, const double* speeds, double dt, int bc,
+                        const double* w, const double* v0, const double* v2, const double* xw,
+                        double* mom_out3, double* rho_out, void* scratch, cudaStream_t st,
+                        size_t* bytes) {
+  switch (p->o * 10 + X->o) {
+#define CASE(A, B)                                                                          \
+  case A * 10 + B:                                                                          \
+    return amr_step<A, B>(p, X, fin, fout, ld, n_cols, speeds, dt, bc, w, v0, v2, xw,       \
+                          mom_out3, rho_out, scratch, st, bytes);
+    CASE(2, 2) CASE(2, 3) CASE(2, 4) CASE(3, 2) CASE(3, 3) CASE(3, 4) CASE(4, 2) CASE(4, 3)
+    CASE(4, 4)
+#undef CASE
+  }
+  set_error("one-pass AMR step: unsupported degrees");
+  return SLDG_ERR_UNSUPPORTED;
+}
+
 // generalized_overlap (vsweep.py:98-122) for one (destination, source) pair: the
 // slow path's own block routine, one thread
 template <int O>
@@ -886,12 +1126,22 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
       for (size_t j = 1; j < qs.size(); ++j) skip[qs[j]] = 1;
     }
   }
+  std::vector<long long> walk_dd_desc;
   for (long long q : walk)
-    if (!skip[q]) walk_dd.push_back(q);
+    if (!skip[q]) {
+      walk_dd.push_back(q);
+      walk_dd_desc.push_back(p_off[q]);
+      walk_dd_desc.push_back((long long)p_n[q] | ((long long)e_level[p_off[q]] << 32));
+    }
   std::vector<long long> t_dd;
   for (long long t = 0; t < T; ++t)
     if (!t_dedup[t]) t_dd.push_back(t);
   if (dd_w.empty()) dd_w.push_back(0.0);
+  std::vector<long long> rest;
+  for (long long e : gen)
+    if (e_slot[e] < 0) rest.push_back(e_row0[e] / nloc);
+  for (long long t : t_dd) rest.push_back(t_row0[t] / nloc);
+  std::sort(rest.begin(), rest.end());
 
   // one device allocation, carved
   struct Piece {
@@ -926,6 +1176,9 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
       {dd_w.data(), sizeof(double) * dd_w.size(), (void**)&p->dev.dd_w},
       {walk_dd.data(), sizeof(long long) * walk_dd.size(), (void**)&p->dev.walk_dd},
       {t_dd.data(), sizeof(long long) * t_dd.size(), (void**)&p->dev.t_dd},
+      {rest.data(), sizeof(long long) * rest.size(), (void**)&p->dev.rest_cells},
+      {walk_dd_desc.data(), sizeof(long long) * walk_dd_desc.size(),
+       (void**)&p->dev.walk_dd_desc},
   };
   size_t total = 0;
   for (auto& pc : pieces) total = align_up(total + pc.bytes, 256);
@@ -966,6 +1219,7 @@ int sldg_vplan_create(const SldgVPlanDesc* d, sldg_vplan** out) {
   p->n_dd_sets = n_dd_sets;
   p->n_walk_dd = (long long)walk_dd.size();
   p->n_targets_dd = (long long)t_dd.size();
+  p->n_rest = (long long)rest.size();
   p->n_dofs = d->n_cells * nloc;
   p->max_pencil_cells = max_cells;
   p->max_walk_cells = max_walk;
@@ -1036,6 +1290,38 @@ int sldg_level_matrices(const sldg_vplan* p, const double* speeds, int64_t n_col
   }
   set_error("unsupported degree");
   return SLDG_ERR_UNSUPPORTED;
+}
+
+int sldg_amr_step_query(const sldg_vplan* p, const sldg_xplan* X, int64_t n_cols, int64_t ld,
+                        size_t* scratch_bytes) {
+  if (!p || !X || !scratch_bytes || n_cols < 1) {
+    set_error("bad amr_step_query arguments");
+    return SLDG_ERR_ARG;
+  }
+  return amr_dispatch(p, X, nullptr, nullptr, ld, n_cols, nullptr, 1.0, SLDG_BC_ABSORBING,
+                      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                      scratch_bytes);
+}
+
+int sldg_amr_step(const sldg_vplan* p, const sldg_xplan* X, const double* fin, double* fout,
+                  int64_t ld, int64_t n_cols, const double* speeds, double dt, int32_t bc,
+                  const double* w, const double* v0, const double* v2, const double* xw,
+                  double* mom_out3, double* rho_out, void* scratch, void* stream) {
+  if (!p || !X || !fin || !fout || fin == fout || !speeds || !w || !v0 || !v2 || !xw ||
+      !mom_out3 || !rho_out || !scratch || n_cols < 1 || ld < n_cols) {
+    set_error("bad amr_step arguments (f_in and f_out must be distinct device buffers)");
+    return SLDG_ERR_ARG;
+  }
+  if (bc != SLDG_BC_PERIODIC && bc != SLDG_BC_ABSORBING) {
+    set_error("boundary mode must be 'periodic' or 'absorbing'");
+    return SLDG_ERR_ARG;
+  }
+  if (!(dt > 0.0)) {
+    set_error("time step must be positive");
+    return SLDG_ERR_ARG;
+  }
+  return amr_dispatch(p, X, fin, fout, ld, n_cols, speeds, dt, bc, w, v0, v2, xw, mom_out3,
+                      rho_out, scratch, (cudaStream_t)stream, nullptr);
 }
 
 int sldg_advect_v(const sldg_vplan* p, const double* fin, double* fout, int64_t ld,

@@ -424,6 +424,32 @@ static int launch_xt(const sldg_xplan* X, const XTGeom& g, const double* fin, do
   return SLDG_ERR_UNSUPPORTED;
 }
 
+// X.X pass (moments of the intermediate, rho of the result) over the velocity cells
+// cells[0 .. n_list), in place: the rows the one-pass AMR step does not finish
+// (amr_fused.cuh).  xx_cells_grid: its CTA count (partials it writes), 0 when the
+// tile kernel cannot run this plan.
+long long xx_cells_grid(const sldg_xplan* X, long long n_list) {
+  if (n_list <= 0) return 0;
+  const long long nloc = (long long)X->vo * X->vo * X->vo;
+  const XTGeom g = xt_geom(X, -1, -1, n_list * nloc);
+  return g.ok ? g.grid_ : 0;
+}
+
+int xx_cells_run(const sldg_xplan* X, double* f, long long ld, const long long* cells,
+                 long long n_list, const double* w, const double* v0, const double* v2,
+                 const double* xw, double* mom_part, double* rho_part, cudaStream_t st) {
+  if (n_list <= 0) return SLDG_OK;
+  const long long nloc = (long long)X->vo * X->vo * X->vo;
+  const XTGeom g = xt_geom(X, -1, -1, n_list * nloc);
+  if (!g.ok) {
+    set_error("cell-list x pass: unsupported geometry");
+    return SLDG_ERR_UNSUPPORTED;
+  }
+  const XEpi epi{w, v0, v2, xw, mom_part, rho_part};
+  const XRowMap rm{g.src_len, 0, 0, 1, 0, ld, 0, cells};
+  return launch_xt(X, g, f, f, ld, 2, true, true, epi, st, &rm);
+}
+
 }  // namespace sldg
 
 using namespace sldg;

@@ -48,10 +48,14 @@ constexpr int kXTMaxTpc = 8;
 // from the row start, halo-relative cell j at src_off + j*o, the local cells are
 // j = hl .. hl+n_xc-1 (no wrap: the halo covers every shift, twice the reach for
 // NAPPLY == 2); outputs go to out_off + cx*o of rows with stride ld_out.  row_off: the
-// absolute first row of the launch (a chunk of whole velocity cells).
+// absolute first row of the launch (a chunk of whole velocity cells).  cells: when set,
+// the launch's velocity cells are cells[0..] (a cell list, e.g. the rows the one-pass
+// AMR step leaves; in place is safe: a tile's rows are staged before they are written
+// and no other tile reads them).
 struct XRowMap {
   int src_len, src_off, hl, wrap, out_off;
   long long ld_out, row_off;
+  const long long* cells;
 };
 
 // RPT > 0: rows per tile fixed at compile time (row loops unrolled, tile -> row
@@ -97,7 +101,8 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
     const int cell = tile / per_cell;
     const int rem = tile - cell * per_cell;
     const int iv = rem % OV, tg = rem / OV;
-    return rm.row_off + (long long)cell * NLOC + tg * rpt * OV + iv;
+    return rm.row_off + (rm.cells ? __ldg(rm.cells + cell) : (long long)cell) * NLOC +
+           tg * rpt * OV + iv;
   };
 
   // a slot is full when warp 0's bulk copies have landed and (epilogues) warp 1's

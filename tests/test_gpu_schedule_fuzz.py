@@ -10,7 +10,8 @@ below runs once with the normal library in this process and twice with the fuzzi
 library in child processes; the results must be bit-identical.  Covered: the fused step
 (lead / steady / last-step modes, field chain cluster) on the headline 64-cell rows,
 the AMR path (stream sweep, per-cell worklist, write-back, X.X tiles), and the x-slab
-pipeline with two ranks in lockstep (halo pack / unpack, slab X.X in chunks).
+pipeline with two ranks in lockstep (halo pack / unpack, slab X.X in chunks), and the
+opt-in one-pass AMR step (one-CTA and four-CTA clusters).
 """
 import hashlib
 import json
@@ -46,6 +47,19 @@ def digests():
         table = sim.advance(4).cpu().numpy()
         f = sim.f.cpu().numpy()
         out[name] = hashlib.sha256(f.tobytes() + table.tobytes()).hexdigest()
+    # the one-pass AMR step (opt-in): bulk-copy ring, per-cell cluster barrier, DSMEM
+    # reads of the peers' slices, bulk stores
+    os.environ["SLDG_AMR_FUSED"] = "on"
+    try:
+        for name, kw in (("amr_onepass", CASES["amr"]),
+                         ("amr_onepass_cluster", dict(dim=3, n_base=4, levels=1, degree=2,
+                                                      n_x=512))):
+            sim = sv.Simulation(sv.SimConfig(**kw, n_steps=4))
+            assert sim.amr_step_supported()
+            table = sim.advance(4).cpu().numpy()
+            out[name] = hashlib.sha256(sim.f.cpu().numpy().tobytes() + table.tobytes()).hexdigest()
+    finally:
+        os.environ.pop("SLDG_AMR_FUSED", None)
     kw = CASES["amr"]
     sims = [shard.ShardedSimulation(sv.SimConfig(**kw, n_steps=3), r, 2, n_chunks=3)
             for r in range(2)]
