@@ -9,8 +9,8 @@
 // are fixed by the row's speed, so every rank packs the same layout: a CSR over rows
 // of the doubles each row sends right (its last w_l cells, the right neighbour's left
 // halo) and left (its first w_r cells).  The exchange itself is the caller's (NCCL
-// send/recv of the packed buffers); these kernels only gather and scatter, coalesced,
-// one warp per row.
+// send/recv of the packed buffers); these kernels only gather and scatter, a few
+// lanes per row.
 #include <algorithm>
 #include <vector>
 
@@ -31,37 +31,46 @@ struct sldg_halo {
 
 namespace sldg {
 
-// rows [r0, r1): a warp per row copies its w cells (w*o doubles, contiguous in both places)
+// rows [r0, r1): a group of L lanes (a power of two <= 32) per row copies its w cells
+// (w*o doubles, contiguous in both places).  L follows the widest row (halo_launch):
+// rows of a few cells (config 4L: <= 24 doubles) leave most of a warp idle behind the
+// row's dependent table loads (row speed -> widths -> CSR offsets), so several rows share
+// a warp; wide rows (config 5: up to 78 doubles) keep a warp each.
 template <bool PACK>
 __global__ void k_halo_copy(const int* __restrict__ row_speed, const int* __restrict__ wl,
                             const int* __restrict__ wr, const long long* __restrict__ off_r,
                             const long long* __restrict__ off_l, int o, long long n_local,
                             double* __restrict__ buf, long long ld, long long lw, long long r0,
-                            long long r1, double* __restrict__ right, double* __restrict__ left) {
-  const int lane = threadIdx.x & 31;
-  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-  const long long base_r = off_r[r0], base_l = off_l[r0];
-  for (long long r = r0 + warp; r < r1; r += nwarps) {
-    const int g = row_speed[r];
-    double* row = buf + r * ld;
-    const int nl = wl[g] * o, nr = wr[g] * o;
-    // left-reaching row: my last nl doubles -> right neighbour; its data -> my left margin
-    double* pr = right + (off_r[r] - base_r);
-    for (int k = lane; k < nl; k += 32) {
+                            long long r1, double* __restrict__ right, double* __restrict__ left,
+                            int lanes) {
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long nt = (long long)gridDim.x * blockDim.x;
+  const int lane = (int)(t0 & (lanes - 1));
+  const long long base_r = __ldg(off_r + r0), base_l = __ldg(off_l + r0);
+  for (long long r = r0 + t0 / lanes; r < r1; r += nt / lanes) {
+  const int g = __ldg(row_speed + r);
+  double* row = buf + r * ld;
+  const int nl = __ldg(wl + g) * o, nr = __ldg(wr + g) * o;
+  // left-reaching row: my last nl doubles -> right neighbour; its data -> my left margin
+  if (nl) {
+    double* pr = right + (__ldg(off_r + r) - base_r);
+    for (int k = lane; k < nl; k += lanes) {
       if (PACK)
         pr[k] = row[lw + n_local * o - nl + k];
       else
         row[lw - nl + k] = pr[k];
     }
-    // right-reaching row: my first nr doubles -> left neighbour; its data -> right margin
-    double* pl = left + (off_l[r] - base_l);
-    for (int k = lane; k < nr; k += 32) {
+  }
+  // right-reaching row: my first nr doubles -> left neighbour; its data -> right margin
+  if (nr) {
+    double* pl = left + (__ldg(off_l + r) - base_l);
+    for (int k = lane; k < nr; k += lanes) {
       if (PACK)
         pl[k] = row[lw + k];
       else
         row[lw + n_local * o + k] = pl[k];
     }
+  }
   }
 }
 
@@ -206,15 +215,21 @@ static int halo_launch(bool pack, const sldg_halo* h, double* buf, int64_t ld, i
     return SLDG_ERR_ARG;
   }
   if (r1 == r0) return SLDG_OK;
-  const long long warps = std::min<long long>(r1 - r0, 148LL * 64);
-  const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
+  // lanes per row: about 4 doubles per lane of the widest row, a power of two <= 32
+  const int widest = std::max(h->reach_l, h->reach_r) * h->o;
+  int lanes = 1;
+  while (lanes < 32 && lanes * 4 < widest) lanes *= 2;
+  const long long threads = std::min<long long>((r1 - r0) * lanes, 148LL * 64 * 32);
+  const unsigned blocks = (unsigned)((threads + 255) / 256);
   cudaStream_t st = (cudaStream_t)stream;
   if (pack)
     k_halo_copy<true><<<blocks, 256, 0, st>>>(h->row_speed, h->wl, h->wr, h->off_r, h->off_l,
-                                              h->o, h->n_local, buf, ld, lw, r0, r1, right, left);
+                                              h->o, h->n_local, buf, ld, lw, r0, r1, right, left,
+                                              lanes);
   else
     k_halo_copy<false><<<blocks, 256, 0, st>>>(h->row_speed, h->wl, h->wr, h->off_r, h->off_l,
-                                               h->o, h->n_local, buf, ld, lw, r0, r1, right, left);
+                                               h->o, h->n_local, buf, ld, lw, r0, r1, right, left,
+                                               lanes);
   SLDG_LAUNCH_CHECK(pack ? "k_halo_pack" : "k_halo_unpack");
   return SLDG_OK;
 }
