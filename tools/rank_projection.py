@@ -30,10 +30,13 @@ ap.add_argument("--config", default="cfg5")
 ap.add_argument("--world", type=int, default=4)
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--kernels", action="store_true", help="also list kernel time per rank-step")
+ap.add_argument("--pencils", action="store_true",
+                help="pencil sharding (PencilShardedSimulation, uniform meshes) instead of x-slabs")
 args = ap.parse_args()
 W, K = args.world, args.steps
 cfg = sv.SimConfig(**bench.CONFIGS[args.config], n_steps=K)
-sims = [shard.ShardedSimulation(cfg, r, W) for r in range(W)]
+cls = shard.PencilShardedSimulation if args.pencils else shard.ShardedSimulation
+sims = [cls(cfg, r, W) for r in range(W)]
 
 
 def timed_lockstep(gens):
@@ -121,6 +124,7 @@ n_v = len(sims[0].vweights)
 dofs = n_v * sims[0].xgrid.n_dofs
 print(json.dumps({
     "config": args.config, "world": W, "steps": K, "phase_dofs": dofs,
+    "sharding": "pencils" if args.pencils else "x-slabs",
     "rank_ms_per_step": [round(t / K, 4) for t in per_rank],
     "max_rank_ms_per_step": round(max(per_rank) / K, 4),
     "exchange_copy_ms_per_step_here": round(exch / K, 4),
