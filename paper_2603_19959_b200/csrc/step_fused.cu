@@ -831,14 +831,54 @@ constexpr int kChainCtas = 8;
 constexpr int kChainThreads = 512;
 constexpr int kChainMaxDofs = 1024;   // x DOFs (and FE nodes) a chain handles
 
-// the 1024-slot tree of the stand-alone reductions, emulated with blockDim threads
-__device__ __forceinline__ double tree1024_sum(double* red) {
-  for (int st = 512; st > 0; st >>= 1) {
-    for (int t = threadIdx.x; t < st; t += blockDim.x) red[t] += red[t + st];
-    __syncthreads();
-  }
-  return red[0];
+#ifdef SLDG_CHAIN_PROF
+// " %d" into buf (device printf of one line per CTA)
+__device__ int snprintf_dev(char* buf, int v) {
+  char t[12];
+  int n = 0;
+  if (v < 0) v = 0;
+  do {
+    t[n++] = (char)('0' + v % 10);
+    v /= 10;
+  } while (v && n < 11);
+  buf[0] = ' ';
+  for (int i = 0; i < n; ++i) buf[1 + i] = t[n - 1 - i];
+  buf[n + 1] = 0;
+  return n + 1;
 }
+#endif
+constexpr int kFoldRegs = 16;
+constexpr int kGreenRegs = 4;   // first Green row's coefficients per lane held in registers   // CTA partials per lane held in registers by the folds
+
+// second half of the cluster barrier the chain arrives at on entry: every CTA of the
+// cluster is running (its shared memory may take DSMEM stores)
+__device__ __forceinline__ void cluster_started() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+
+// The 1024-slot tree of the stand-alone reductions (for st = 512 .. 1: red[t] op=
+// red[t + st], t < st) in one warp with no barriers: lane l first combines the 32 slots
+// l + 32 k with the tree's own pairs (levels 512 .. 32: k op= k + 16, 8, 4, 2, 1), then
+// levels 16 .. 1 by shuffles.  Same operands in the same order: bitwise identical.
+template <typename Val, typename Op>
+__device__ __forceinline__ double warp_tree1024(int lane, Val val, Op op) {
+  double v[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = val(lane + 32 * k);
+#pragma unroll
+  for (int h = 16; h > 0; h >>= 1)
+#pragma unroll
+    for (int k = 0; k < h; ++k) v[k] = op(v[k], v[k + h]);
+  double r = v[0];
+#pragma unroll
+  for (int st = 16; st > 0; st >>= 1) {
+    const double o = __shfl_down_sync(0xffffffffu, r, st);
+    r = op(r, o);
+  }
+  return __shfl_sync(0xffffffffu, r, 0);
+}
+
 
 template <int O>
 __global__ void __cluster_dims__(kChainCtas, 1, 1) __launch_bounds__(kChainThreads, 1)
@@ -853,8 +893,8 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
               double* __restrict__ lm_mats) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
-  __shared__ double r_s[kChainMaxDofs], phi_s[kChainMaxDofs], e_s[kChainMaxDofs];
-  __shared__ double red[1024], red2[1024];
+  __shared__ double r_s[kChainMaxDofs], phi_s[kChainMaxDofs], phx[kChainMaxDofs],
+      e_s[kChainMaxDofs], xw_s[kChainMaxDofs], diff_s[kMaxO * kMaxO];
   const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, nw = blockDim.x >> 5;
   const int rank = (int)cluster.block_rank();
   const int o = p + 1;
@@ -864,131 +904,175 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
   const int q0 = share(nn, rank), q1 = share(nn, rank + 1);     // my FE rows
   // PDL: wait for the preceding fused step (its partials and state are complete),
   // then let the next fused step start its E-independent prologue alongside us
+  // -DSLDG_CHAIN_PROF: global-timer stamps between the stages, printed by CTAs 0 and 1
+#ifdef SLDG_CHAIN_PROF
+  unsigned long long tst[10];
+  int nst = 0;
+#define CHAIN_STAMP() asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tst[nst++]))
+#else
+#define CHAIN_STAMP() do {} while (0)
+#endif
+  CHAIN_STAMP();
+  // DSMEM stores need the peer CTAs running: arrive now, wait before the first push
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  // the plan's constants (x weights, derivative matrix, my first Green row) before the
+  // dependency wait: they overlap the preceding fused step's tail
+  for (int t = tid; t < nd; t += blockDim.x) xw_s[t] = __ldg(pxw + t);
+  if (tid < o * o) diff_s[tid] = __ldg(diff + tid);
+  const int row0 = q0 + wp;
+  double gr[kGreenRegs];
+#pragma unroll
+  for (int i = 0; i < kGreenRegs; ++i) {
+    const int k = lane + 32 * i;
+    gr[i] = (row0 < q1 && k < nn) ? __ldg(green + (size_t)row0 * nn + k) : 0.0;
+  }
   grid_dep_wait();
   grid_dep_launch();
+  CHAIN_STAMP();
   if (!rho_in) {
-    for (int c = c0 + wp; c < c1; c += nw) {
-      const double* q = rho_part + (size_t)c * np;
-      double sacc = 0.0;
-#pragma unroll 4
-      for (int k = lane; k < np; k += 32) sacc += __ldg(q + k);
+    // fold (k_fold_cols / k_fold3 order: lane l sums partials l, l+32, ... in sequence,
+    // then the xor butterfly); every load of a warp's columns is issued before the sums
+    // (one L2 round trip instead of one per four partials per column)
+    for (int ca = c0 + wp; ca < c1; ca += 2 * nw) {
+      const int cb = ca + nw;
+      const bool hb = cb < c1;
+      const double* qa = rho_part + (size_t)ca * np;
+      const double* qb = rho_part + (size_t)(hb ? cb : ca) * np;
+      double va[kFoldRegs], vb[kFoldRegs];
 #pragma unroll
-      for (int of = 16; of > 0; of >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, of);
+      for (int i = 0; i < kFoldRegs; ++i) {
+        const int k = lane + 32 * i;
+        va[i] = k < np ? __ldg(qa + k) : 0.0;
+        vb[i] = (hb && k < np) ? __ldg(qb + k) : 0.0;
+      }
+      double sa = 0.0, sb = 0.0;
+#pragma unroll
+      for (int i = 0; i < kFoldRegs; ++i)
+        if (lane + 32 * i < np) {
+          sa += va[i];
+          sb += vb[i];
+        }
+      for (int k = lane + 32 * kFoldRegs; k < np; k += 32) {
+        sa += __ldg(qa + k);
+        sb += __ldg(qb + k);
+      }
+#pragma unroll
+      for (int of = 16; of > 0; of >>= 1) {
+        sa += __shfl_xor_sync(0xffffffffu, sa, of);
+        sb += __shfl_xor_sync(0xffffffffu, sb, of);
+      }
       if (lane == 0) {
-        rho[c] = sacc;
-        r_s[c] = sacc;
+        rho[ca] = sa;
+        r_s[ca] = sa;
+        if (hb) {
+          rho[cb] = sb;
+          r_s[cb] = sb;
+        }
       }
     }
-    if (rank == 0 && mom_prev && wp < 3) {
+    // moments (k_fold3 order) on the last three warps of CTA 0 (they fold fewer columns)
+    const int mw = wp - (nw - 3);
+    if (rank == 0 && mom_prev && mw >= 0) {
+      double v[kFoldRegs];
+#pragma unroll
+      for (int i = 0; i < kFoldRegs; ++i) {
+        const int k = lane + 32 * i;
+        v[i] = k < np ? __ldg(mom_part + (size_t)k * 3 + mw) : 0.0;
+      }
       double sacc = 0.0;
-      for (long long k = lane; k < n_parts; k += 32) sacc += mom_part[k * 3 + wp];
+#pragma unroll
+      for (int i = 0; i < kFoldRegs; ++i)
+        if (lane + 32 * i < np) sacc += v[i];
+      for (int k = lane + 32 * kFoldRegs; k < np; k += 32) sacc += mom_part[(size_t)k * 3 + mw];
 #pragma unroll
       for (int of = 16; of > 0; of >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, of);
-      if (lane == 0) mom_prev[wp] = sacc;
+      if (lane == 0) mom_prev[mw] = sacc;
+    }
+    CHAIN_STAMP();
+    // my columns pushed into the shared rho of every CTA (no gather after the barrier)
+    cluster_started();
+    __syncthreads();
+    for (int k = tid; k < (c1 - c0) * kChainCtas; k += blockDim.x) {
+      const int c = c0 + k / kChainCtas, dst = k % kChainCtas;
+      if (dst != rank) *cluster.map_shared_rank(&r_s[c], dst) = r_s[c];
     }
     fuzz_delay();
-    cluster.sync();
-    for (int c = tid; c < nd; c += blockDim.x) {
-      if (c >= c0 && c < c1) continue;
-      int owner = 0;
-      while (c >= share(nd, owner + 1)) ++owner;
-      r_s[c] = *cluster.map_shared_rank(&r_s[c], owner);
-    }
+    cluster.sync();   // every CTA's columns are in every r_s
+    CHAIN_STAMP();
   } else {
+    cluster_started();
     for (int c = tid; c < nd; c += blockDim.x) r_s[c] = rho_in[c];
+    __syncthreads();
   }
-  // Poisson right-hand side (k_poisson_rhs): fma(w, r, 0) per slot, 1024-slot tree
-  for (int t = tid; t < 1024; t += blockDim.x) red[t] = t < nd ? fma(pxw[t], r_s[t], 0.0) : 0.0;
-  __syncthreads();
-  const double rbar = tree1024_sum(red) / length;
+  // Poisson right-hand side (k_poisson_rhs): fma(w, r, 0) per slot, the 1024-slot tree,
+  // evaluated by every warp on its own (warp_tree1024: same pairs, same order)
+  const double rbar = warp_tree1024(lane, [&](int t) {
+    return t < nd ? fma(xw_s[t], r_s[t], 0.0) : 0.0;
+  }, [](double x, double y) { return x + y; }) / length;
   for (int node = tid; node < nn; node += blockDim.x) {
     const int cell = node / p, j = node - cell * p;
     double v;
     if (j == 0) {
       const int kprev = (cell == 0 ? (int)n_cells - 1 : cell - 1) * o + p, kthis = cell * o;
-      const double cprev = __dmul_rn(pxw[kprev], __dsub_rn(r_s[kprev], rbar));
-      const double cthis = __dmul_rn(pxw[kthis], __dsub_rn(r_s[kthis], rbar));
+      const double cprev = __dmul_rn(xw_s[kprev], __dsub_rn(r_s[kprev], rbar));
+      const double cthis = __dmul_rn(xw_s[kthis], __dsub_rn(r_s[kthis], rbar));
       v = (cell == 0) ? __dadd_rn(cthis, cprev) : __dadd_rn(cprev, cthis);
     } else {
       const int k = cell * o + j;
-      v = __dmul_rn(pxw[k], __dsub_rn(r_s[k], rbar));
+      v = __dmul_rn(xw_s[k], __dsub_rn(r_s[k], rbar));
     }
     phi_s[node] = v;   // b, staged for the GEMV
     if (rank == 0) b[node] = v;
   }
   __syncthreads();
-  // phi = G b (k_gemv: warp per row), my rows; b lives in phi_s until the rows are done
-  double rowv[kChainMaxDofs / (kChainCtas * 16) + 1];
-  int nrow = 0;
-  for (int row = q0 + wp; row < q1; row += nw) {
+  CHAIN_STAMP();
+  // phi = G b (k_gemv: warp per row, lane-strided FMA chain, xor butterfly), my rows,
+  // each pushed into every CTA's phx (phi_s holds b until every GEMV is done)
+  for (int row = row0; row < q1; row += nw) {
     double t = 0.0;
     const double* g = green + (size_t)row * nn;
+    int k = lane;
+    if (row == row0) {
+#pragma unroll
+      for (int i = 0; i < kGreenRegs; ++i, k += 32)
+        if (k < nn) t = fma(gr[i], phi_s[k], t);
+    }
 #pragma unroll 4
-    for (int k = lane; k < nn; k += 32) t = fma(__ldg(g + k), phi_s[k], t);
+    for (; k < nn; k += 32) t = fma(__ldg(g + k), phi_s[k], t);
 #pragma unroll
     for (int of = 16; of > 0; of >>= 1) t += __shfl_xor_sync(0xffffffffu, t, of);
-    rowv[nrow++] = t;
-  }
-  __syncthreads();
-  nrow = 0;
-  for (int row = q0 + wp; row < q1; row += nw) {
-    const double t = rowv[nrow++];
-    if (lane == 0) {
-      phi_s[row] = t;
-      phi[row] = t;
-    }
+    if (lane == 0) phi[row] = t;
+    if (lane < kChainCtas) *cluster.map_shared_rank(&phx[row], lane) = t;
   }
   fuzz_delay();
-  cluster.sync();
-  for (int node = tid; node < nn; node += blockDim.x) {
-    if (node >= q0 && node < q1) continue;
-    int owner = 0;
-    while (node >= share(nn, owner + 1)) ++owner;
-    red2[node] = *cluster.map_shared_rank(&phi_s[node], owner);
-  }
-  __syncthreads();
-  for (int node = tid; node < nn; node += blockDim.x)
-    if (node < q0 || node >= q1) phi_s[node] = red2[node];
-  __syncthreads();
-  // E (k_efield), my DOFs
+  cluster.sync();   // phi complete everywhere; no shared memory access across CTAs after this
+  CHAIN_STAMP();
+  // E (k_efield) at every DOF in every CTA (each CTA stores its own DOFs)
   const double sc = -(2.0 / h);
-  for (int k = c0 + tid; k < c1; k += blockDim.x) {
+  for (int k = tid; k < nd; k += blockDim.x) {
     const int cell = k / o, i = k - cell * o;
     double t = 0.0;
     for (int j = 0; j < o; ++j) {
       const int node = (cell * p + j) % nn;
-      t = fma(__dmul_rn(sc, phi_s[node]), diff[i * o + j], t);
+      t = fma(__dmul_rn(sc, phx[node]), diff_s[i * o + j], t);
     }
     e_s[k] = t;
-    e[k] = t;
+    if (k >= c0 && k < c1) e[k] = t;
   }
-  fuzz_delay();
-  cluster.sync();
-  if (rank == 0) {
-    // field diagnostics (k_field_diag): max |E| and 0.5 w.E^2, 1024-slot trees
-    for (int k = tid; k < nd; k += blockDim.x) {
-      if (k >= c0 && k < c1) continue;
-      int owner = 0;
-      while (k >= share(nd, owner + 1)) ++owner;
-      e_s[k] = *cluster.map_shared_rank(&e_s[k], owner);
-    }
-    __syncthreads();
-    for (int t = tid; t < 1024; t += blockDim.x) {
+  __syncthreads();
+  CHAIN_STAMP();
+  if (rank == 0 && wp == nw - 1) {
+    // field diagnostics (k_field_diag): max |E| and 0.5 w.E^2, the 1024-slot trees
+    const double emax = warp_tree1024(lane, [&](int t) {
+      return t < nd ? fmax(0.0, fabs(e_s[t])) : 0.0;
+    }, [](double x, double y) { return fmax(x, y); });
+    const double ee = warp_tree1024(lane, [&](int t) {
       const double v = t < nd ? e_s[t] : 0.0;
-      red[t] = t < nd ? fmax(0.0, fabs(v)) : 0.0;
-      red2[t] = t < nd ? fma(pxw[t], v * v, 0.0) : 0.0;
-    }
-    __syncthreads();
-    for (int st = 512; st > 0; st >>= 1) {
-      for (int t = tid; t < st; t += blockDim.x) {
-        red[t] = fmax(red[t], red[t + st]);
-        red2[t] += red2[t + st];
-      }
-      __syncthreads();
-    }
-    if (tid == 0) {
-      diag2[0] = red[0];
-      diag2[1] = 0.5 * red2[0];
+      return t < nd ? fma(xw_s[t], v * v, 0.0) : 0.0;
+    }, [](double x, double y) { return x + y; });
+    if (lane == 0) {
+      diag2[0] = emax;
+      diag2[1] = 0.5 * ee;
     }
   }
   // level matrices for speeds = E (k_level_mats): my columns, one thread per
@@ -1022,8 +1106,15 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
     for (int k = 0; k < O * O; ++k)
       lm_mats[((long long)(lev * 2 + ab) * O * O + k) * nd + c] = M[k];
   }
-  fuzz_delay();
-  cluster.sync();   // no CTA leaves while another may still read its shared memory
+#ifdef SLDG_CHAIN_PROF
+  CHAIN_STAMP();
+  if (tid == 0 && rank < 2) {
+    char buf[160];
+    int n = 0;
+    for (int k = 1; k < nst; ++k) n += snprintf_dev(buf + n, (int)tst[k] - (int)tst[k - 1]);
+    printf("chain rank %d:%s\n", rank, buf);
+  }
+#endif
 }
 
 }  // namespace sldg
