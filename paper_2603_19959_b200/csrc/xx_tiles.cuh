@@ -65,6 +65,8 @@ __global__ void __launch_bounds__(512, 1)
 k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout, long long ld,
            long long n_rows, int n_xc, int rpt_arg, int tpc, int nring, int n_speeds, XEpi epi,
            int napply, int mom, int rho, XRowMap rm) {
+  const int wrap = rm.wrap;
+  const long long* cells = rm.cells;
   constexpr int NL = OV * OV, NLOC = NL * OV;
   constexpr int XM = 2 * OX * OX;
   const int rpt = RPT > 0 ? RPT : rpt_arg;
@@ -84,7 +86,8 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
   double* ring = sm;
   double* mid = ring + (long long)nring * slot_dbl;
   double* meta = mid + slot_dbl;             // [nring][tpc][rpt][3]: w, w*v0, w*v2
-  double* xtab = meta + (long long)nring * tpc * rpt * 3;   // per speed: A | B
+  // per speed: A | B (2 OX^2 doubles: 16-byte aligned blocks, read as pairs)
+  double* xtab = meta + (((long long)nring * tpc * rpt * 3 + 1) & ~1LL);
   int* xnsm = reinterpret_cast<int*>(xtab + (long long)n_speeds * XM);
   // a zero shift is stored as (A, B) = (I, 0) with no cell shift, so the update has
   // no per-thread branch (1*u0 + 0*u1 + ... == u0)
@@ -94,14 +97,14 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
   }
   // periodic rows: the shift mod n_xc; slabs: the true shift (the halo covers it)
   for (int k = tid; k < n_speeds; k += blockDim.x)
-    xnsm[k] = X.ident[k] ? 0 : (rm.wrap ? __ldg(X.nsm + k) : (int)__ldg(X.ns + k));
+    xnsm[k] = X.ident[k] ? 0 : (wrap ? __ldg(X.nsm + k) : (int)__ldg(X.ns + k));
 
   // tile id -> first row and row stride (rows u = 0..rpt-1 are row0 + u*OV)
   auto tile_row0 = [&](int tile) -> long long {
     const int cell = tile / per_cell;
     const int rem = tile - cell * per_cell;
     const int iv = rem % OV, tg = rem / OV;
-    return rm.row_off + (rm.cells ? __ldg(rm.cells + cell) : (long long)cell) * NLOC +
+    return rm.row_off + (cells ? __ldg(cells + cell) : (long long)cell) * NLOC +
            tg * rpt * OV + iv;
   };
 
@@ -172,11 +175,12 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
       row0 = tile_row0(tile);
       const double* AB = xtab + (long long)g * XM;
 #pragma unroll
-      for (int k = 0; k < OX * OX; ++k) {
-        xa[k] = AB[k];
-        xb[k] = AB[OX * OX + k];
+      for (int k = 0; k < XM; k += 2) {
+        const double2 q = *reinterpret_cast<const double2*>(AB + k);
+        (k < OX * OX ? xa[k] : xb[k - OX * OX]) = q.x;
+        (k + 1 < OX * OX ? xa[k + 1] : xb[k + 1 - OX * OX]) = q.y;
       }
-      if (rm.wrap) {
+      if (wrap) {
         int a = cx - xnsm[g];   // nsm in [0, n_xc): the periodic source cell of cx
         if (a < 0) a += n_xc;
         ia = a * OX;
@@ -215,15 +219,15 @@ k_xx_tiles(XPlanDev X, const double* __restrict__ fin, double* __restrict__ fout
         // beyond the local ones (left of them for n >= 0, right for n < 0); thread cx
         // forms local cell cx (moments as on periodic rows) and, for cx < extra, one of
         // those halo cells (sources within the doubled halo)
-        const int nsh = rm.wrap ? 0 : xnsm[g];
-        const int extra = rm.wrap ? 0 : (nsh >= 0 ? nsh + 1 : -nsh);
+        const int nsh = wrap ? 0 : xnsm[g];
+        const int extra = wrap ? 0 : (nsh >= 0 ? nsh + 1 : -nsh);
         const int xcell = nsh >= 0 ? rm.hl - 1 - cx : rm.hl + n_xc + cx;   // halo-relative
         const int xa_ = rm.src_off + (xcell - nsh) * OX;
 #pragma unroll(RPT > 0 ? RPT : 1)
         for (int u = 0; u < rpt; ++u) {
           double y[OX];
           xapply(src + u * src_len, y);
-          const int mo = rm.wrap ? cx * OX : rm.src_off + (rm.hl + cx) * OX;
+          const int mo = wrap ? cx * OX : rm.src_off + (rm.hl + cx) * OX;
 #pragma unroll
           for (int k = 0; k < OX; ++k) md[u * src_len + mo + k] = y[k];
           if (cx < extra) {
