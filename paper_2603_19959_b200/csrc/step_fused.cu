@@ -827,7 +827,10 @@ static FusedScratch fused_scratch(const sldg_vplan* vp, const FusedGeom& g, long
 //   E        DOFs split over the CTAs (k_efield); CTA 0 gathers E for the diagnostics
 //            (the 1024-slot trees of k_field_diag) while every CTA forms the level
 //            matrices of its columns, one thread per (level, column, A|B).
-constexpr int kChainCtas = 8;
+#ifndef SLDG_CHAIN_CTAS
+#define SLDG_CHAIN_CTAS 8
+#endif
+constexpr int kChainCtas = SLDG_CHAIN_CTAS;   // CTAs of the field chain cluster
 constexpr int kChainThreads = 512;
 constexpr int kChainMaxDofs = 1024;   // x DOFs (and FE nodes) a chain handles
 
