@@ -905,8 +905,6 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
   auto share = [&](int n, int r) { return (int)((long long)n * r / kChainCtas); };
   const int c0 = share(nd, rank), c1 = share(nd, rank + 1);     // my columns / DOFs
   const int q0 = share(nn, rank), q1 = share(nn, rank + 1);     // my FE rows
-  // PDL: wait for the preceding fused step (its partials and state are complete),
-  // then let the next fused step start its E-independent prologue alongside us
   // -DSLDG_CHAIN_PROF: global-timer stamps between the stages, printed by CTAs 0 and 1
 #ifdef SLDG_CHAIN_PROF
   unsigned long long tst[10];
@@ -929,6 +927,8 @@ k_field_chain(const double* __restrict__ rho_in, const double* __restrict__ rho_
     const int k = lane + 32 * i;
     gr[i] = (row0 < q1 && k < nn) ? __ldg(green + (size_t)row0 * nn + k) : 0.0;
   }
+  // PDL: wait for the preceding fused step (its partials and state are complete),
+  // then let the next fused step start its E-independent prologue alongside us
   grid_dep_wait();
   grid_dep_launch();
   CHAIN_STAMP();
